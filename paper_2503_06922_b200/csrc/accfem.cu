@@ -1,0 +1,501 @@
+// B200 (sm_100a) device library behind include/accfem.h.
+//
+// Kernels (all FP64, one warp = one scenario, persistent over a dynamic
+// scenario queue):
+//   k_model_setup     per-model constants (once per handle)
+//   k_solve           run_static / step for a batch: element pass, detection,
+//                     assembly, Ruiz, block Cholesky, ADMM, polish, update
+//   k_element_pass    unit entry point: F_int + block-tridiagonal K
+//   k_detect          unit entry point: per-node contact winner
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/accfem.h"
+#include "engine.cuh"
+#include "host_build.hpp"
+
+using namespace accfem;
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+
+__global__ void k_model_setup(int N, const double* rest, double* rest_dir, double* rest_len, double* rest_frames,
+                              double* offsets, double* qa, double* qb, int* bad) {
+  TeamWarp team{(int)(threadIdx.x & 31)};
+  if (threadIdx.x >= 32) return;
+  model_setup(team, N, rest, rest_dir, rest_len, rest_frames, offsets, qa, qb, bad);
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride) {
+  TeamWarp team{(int)(threadIdx.x & 31)};
+  const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, B.cmax_polish);
+  while (true) {
+    int s = 0;
+    if (team.lane == 0) s = atomicAdd(B.work_counter, 1);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (s >= B.S) break;
+    run_scenario(team, P, B, s, ws);
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_element_pass(Problem P, int S, const double* x, double* fint, double* kd, double* ku, double* frames, int* bad,
+                   double* ws_base, long ws_stride, int* counter) {
+  TeamWarp team{(int)(threadIdx.x & 31)};
+  const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, 1);
+  const int N = P.m.N, n = 6 * N, E = N - 1;
+  while (true) {
+    int s = 0;
+    if (team.lane == 0) s = atomicAdd(counter, 1);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (s >= S) break;
+    int b = element_pass(team, P, x + (long)s * n, ws, true);
+    if (team.lane == 0 && bad) bad[s] = b;
+    if (b) continue;
+    for (int i = team.lane; i < n; i += 32) fint[(long)s * n + i] = ws.fint[i];
+    if (kd)
+      for (int i = team.lane; i < 36 * N; i += 32) kd[(long)s * 36 * N + i] = ws.KD[i];
+    if (ku)
+      for (int i = team.lane; i < 36 * E; i += 32) ku[(long)s * 36 * E + i] = ws.KU[i];
+    if (frames)
+      for (int i = team.lane; i < 9 * E; i += 32) frames[(long)s * 9 * E + i] = ws.frames[i];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_detect(Problem P, int S, const double* x, int* tri, double* gap, double* point, double* ws_base, long ws_stride,
+             int* counter) {
+  TeamWarp team{(int)(threadIdx.x & 31)};
+  const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, 1);
+  const int N = P.m.N, n = 6 * N;
+  while (true) {
+    int s = 0;
+    if (team.lane == 0) s = atomicAdd(counter, 1);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (s >= S) break;
+    int nc = detect_pass(team, P, x + (long)s * n, ws);
+    // scatter back to node order: -1 for nodes without a contact
+    for (int k = team.lane; k < N; k += 32) tri[(long)s * N + k] = -1;
+    __syncwarp();
+    for (int c = team.lane; c < nc; c += 32) {
+      int k = ws.cnode[c];
+      tri[(long)s * N + k] = ws.ctri[c];
+      gap[(long)s * N + k] = ws.cgap[c];
+      for (int a = 0; a < 3; ++a) point[((long)s * N + k) * 3 + a] = ws.cpp[3 * c + a];
+    }
+    __syncwarp();
+  }
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    if (count <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  cudaError_t upload(const T* h, size_t count) {
+    cudaError_t e = alloc(count);
+    if (e != cudaSuccess) return e;
+    if (count) return cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice);
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct accfem_handle {
+  int device = 0;
+  int sms = 0;
+  int blocks_per_sm = 0;
+  int launches = 0;
+  std::string err;
+  Problem P;
+  int n_cables = 0, n_fixed = 0, N = 0, cmax = 0;
+  DevBuf<double> rest, rest_dir, rest_len, rest_frames, offsets, qa, qb, fixed_inc;
+  DevBuf<int> fixed_node, fixed_dof, fixed_row_of_dof, bad;
+  DevBuf<double> corners, normals, lo, hi;
+  DevBuf<int> tri_cell_lo, cell_start, cell_tris;
+  DevBuf<double> ws;
+  DevBuf<int> counter;
+  long ws_stride = 0;
+  // host-path staging (accfem_solve_batch_host)
+  DevBuf<double> h_x0, h_ten, h_app, h_ins, h_wy, h_wf, h_rho, o_coords, o_res, o_cd, o_wy, o_wf, o_rho, o_tr;
+  DevBuf<int> o_ints;
+};
+
+static int fail(accfem_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+#define CUDA_OK(h, expr)                                                                  \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) return fail((h), ACCFEM_E_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+static thread_local std::string g_create_error;
+
+extern "C" int accfem_version(void) { return 1; }
+
+extern "C" const char* accfem_last_error(const accfem_handle* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc* mesh, const accfem_settings* sd,
+                             int device, accfem_handle** out) {
+  g_create_error.clear();
+  if (!out) return ACCFEM_E_ARG;
+  *out = nullptr;
+  std::string v = accfem_host::validate(md, sd);
+  if (!v.empty()) {
+    g_create_error = v;
+    return ACCFEM_E_DOMAIN;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    return ACCFEM_E_CUDA;
+  }
+  accfem_handle* h = new accfem_handle();
+  h->device = device;
+  const int N = md->node_count, E = N - 1;
+  h->N = N;
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+  Problem& P = h->P;
+  memset(&P, 0, sizeof(P));
+  // settings
+  Settings& S = P.s;
+  S.eps_abs = sd->eps_abs; S.eps_rel = sd->eps_rel; S.rho = sd->rho; S.sigma = sd->sigma;
+  S.alpha = sd->alpha; S.beta0 = sd->beta0; S.margin = sd->margin;
+  S.radius = std::max(sd->margin + sd->beta0, sd->margin);
+  S.max_iterations = sd->max_iterations; S.check_interval = sd->check_interval;
+  S.adaptive_rho = sd->adaptive_rho; S.scaling_iterations = sd->scaling_iterations; S.polish = sd->polish;
+  h->cmax = sd->polish_capacity > 0 ? sd->polish_capacity : std::min(N, 256);
+  // model
+  ModelDev& M = P.m;
+  M.N = N;
+  M.l0 = md->element_rest_length;
+  accfem_host::local_stiffness(md, M.kl);
+  M.n_cables = sd->n_cables;
+  h->n_cables = sd->n_cables;
+  for (int j = 0; j < sd->n_cables; ++j)
+    for (int a = 0; a < 3; ++a) {
+      M.cable_off[3 * j + a] = sd->cable_offset[3 * j + a];
+      M.cable_dir[3 * j + a] = sd->cable_direction[3 * j + a];
+    }
+  {
+    const double* r = md->rest_coords;
+    double ax[3] = {r[6] - r[0], r[7] - r[1], r[8] - r[2]};
+    double nrm = sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+    for (int a = 0; a < 3; ++a) M.axis[a] = ax[a] / nrm;
+  }
+  M.has_uniform = sd->has_uniform_load;
+  for (int a = 0; a < 3; ++a) M.uniform[a] = sd->uniform_load[a];
+  M.n_fixed = sd->n_fixed;
+  h->n_fixed = sd->n_fixed;
+  std::vector<int> frd(6L * N, -1);
+  for (int r = 0; r < sd->n_fixed; ++r) frd[6 * sd->fixed_node[r] + sd->fixed_dof[r]] = r;
+  int rc = 0;
+#define UP(buf, ptr, cnt) \
+  if ((e = h->buf.upload((ptr), (cnt))) != cudaSuccess) { rc = 1; }
+  UP(rest, md->rest_coords, 6L * N);
+  UP(fixed_node, sd->fixed_node, sd->n_fixed);
+  UP(fixed_dof, sd->fixed_dof, sd->n_fixed);
+  UP(fixed_inc, sd->fixed_increment, sd->n_fixed);
+  UP(fixed_row_of_dof, frd.data(), frd.size());
+  if (!rc) {
+    h->rest_dir.alloc(9L * N); h->rest_len.alloc(E); h->rest_frames.alloc(9L * E);
+    h->offsets.alloc(9L * E); h->qa.alloc(9L * E); h->qb.alloc(9L * E); h->bad.alloc(1);
+  }
+  // mesh + grid
+  accfem_host::HostMesh hm;
+  std::string merr = accfem_host::build_mesh(mesh, S.radius, hm);
+  if (!merr.empty()) {
+    g_create_error = merr;
+    delete h;
+    return ACCFEM_E_MESH;
+  }
+  if (hm.T > 0) {
+    UP(corners, hm.corners.data(), hm.corners.size());
+    UP(normals, hm.normals.data(), hm.normals.size());
+    UP(lo, hm.lo.data(), hm.lo.size());
+    UP(hi, hm.hi.data(), hm.hi.size());
+    UP(tri_cell_lo, hm.tri_cell_lo.data(), hm.tri_cell_lo.size());
+    UP(cell_start, hm.cell_start.data(), hm.cell_start.size());
+    UP(cell_tris, hm.cell_tris.data(), hm.cell_tris.size());
+  }
+#undef UP
+  if (rc || h->counter.alloc(4) != cudaSuccess) {
+    g_create_error = std::string("device allocation failed: ") + cudaGetErrorString(e);
+    delete h;
+    return ACCFEM_E_CUDA;
+  }
+  MeshDev& G = P.mesh;
+  G.T = hm.T;
+  G.corners = h->corners.p; G.normals = h->normals.p; G.lo = h->lo.p; G.hi = h->hi.p;
+  G.tri_cell_lo = h->tri_cell_lo.p; G.cell_start = h->cell_start.p; G.cell_tris = h->cell_tris.p;
+  for (int a = 0; a < 3; ++a) {
+    G.origin[a] = hm.origin[a];
+    G.dims[a] = hm.dims[a];
+  }
+  G.inv_h = hm.inv_h;
+  M.rest_dir = h->rest_dir.p; M.rest_len = h->rest_len.p; M.rest_frames = h->rest_frames.p;
+  M.offsets = h->offsets.p; M.qa = h->qa.p; M.qb = h->qb.p;
+  M.fixed_node = h->fixed_node.p; M.fixed_dof = h->fixed_dof.p; M.fixed_inc = h->fixed_inc.p;
+  M.fixed_row_of_dof = h->fixed_row_of_dof.p;
+  // per-model constants on the device
+  k_model_setup<<<1, 32>>>(N, h->rest.p, h->rest_dir.p, h->rest_len.p, h->rest_frames.p, h->offsets.p, h->qa.p,
+                           h->qb.p, h->bad.p);
+  h->launches++;
+  int bad = 0;
+  e = cudaMemcpy(&bad, h->bad.p, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    g_create_error = std::string("model setup: ") + cudaGetErrorString(e);
+    delete h;
+    return ACCFEM_E_CUDA;
+  }
+  if (bad) {
+    g_create_error = "rest configuration has coincident nodes";
+    delete h;
+    return ACCFEM_E_DOMAIN;
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kWarpsPerBlock, 0);
+  if (h->blocks_per_sm < 1) h->blocks_per_sm = 1;
+  *out = h;
+  return 0;
+}
+
+extern "C" int accfem_destroy(accfem_handle* h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  for (auto* b : {&h->rest, &h->rest_dir, &h->rest_len, &h->rest_frames, &h->offsets, &h->qa, &h->qb, &h->fixed_inc,
+                  &h->corners, &h->normals, &h->lo, &h->hi, &h->ws, &h->h_x0, &h->h_ten, &h->h_app, &h->h_ins,
+                  &h->h_wy, &h->h_wf, &h->h_rho, &h->o_coords, &h->o_res, &h->o_cd, &h->o_wy, &h->o_wf, &h->o_rho,
+                  &h->o_tr})
+    b->release();
+  for (auto* b : {&h->fixed_node, &h->fixed_dof, &h->fixed_row_of_dof, &h->bad, &h->tri_cell_lo, &h->cell_start,
+                  &h->cell_tris, &h->counter, &h->o_ints})
+    b->release();
+  delete h;
+  return 0;
+}
+
+// size the workspace for `teams` resident warps
+static int ensure_ws(accfem_handle* h, long teams, int cmax) {
+  long stride = ws_doubles(h->N, cmax);
+  stride = (stride + 31) & ~31L;
+  size_t need = (size_t)stride * teams;
+  if (h->ws_stride != stride || h->ws.n < need) {
+    h->ws.release();
+    CUDA_OK(h, h->ws.alloc(need));
+    h->ws_stride = stride;
+  }
+  return 0;
+}
+
+static long grid_blocks(accfem_handle* h, long S) {
+  long want = (S + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  long cap = (long)h->sms * h->blocks_per_sm;
+  return std::max(1L, std::min(want, cap));
+}
+
+extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm * kWarpsPerBlock : 0; }
+extern "C" long long accfem_workspace_bytes(accfem_handle* h) { return h ? (long long)h->ws.n * 8 : 0; }
+extern "C" int accfem_launches(accfem_handle* h) { return h ? h->launches : 0; }
+
+extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void* stream) {
+  if (!h || !io) return ACCFEM_E_ARG;
+  if (io->S <= 0) return 0;
+  if (!io->x0 || !io->coords || !io->status || !io->frames || !io->converged || !io->residual || !io->n_contacts ||
+      !io->contact_node || !io->contact_triangle || !io->contact_gap || !io->contact_multiplier ||
+      !io->contact_force || !io->contact_normal || !io->contact_point)
+    return fail(h, ACCFEM_E_ARG, "missing required batch buffer");
+  if (io->max_frames < 1) return fail(h, ACCFEM_E_ARG, "max_frames must be >= 1");
+  if (h->n_cables > 0 && io->tensions == nullptr) {
+    // tensions None: no cable wrench (engine.py:111)
+  }
+  CUDA_OK(h, cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  long blocks = grid_blocks(h, io->S);
+  if (int rc = ensure_ws(h, blocks * kWarpsPerBlock, h->cmax)) return rc;
+  BatchDev B;
+  memset(&B, 0, sizeof(B));
+  B.S = io->S;
+  B.x0 = io->x0; B.tensions = h->n_cables ? io->tensions : nullptr; B.applied = io->applied;
+  B.insertion = io->insertion; B.warm_y_in = io->warm_y_in; B.warm_fix_in = io->warm_fixed_in; B.rho_in = io->rho_in;
+  B.coords = io->coords; B.status = io->status; B.frames = io->frames; B.converged = io->converged;
+  B.residual = io->residual; B.n_contacts = io->n_contacts; B.c_node = io->contact_node;
+  B.c_tri = io->contact_triangle; B.c_gap = io->contact_gap; B.c_y = io->contact_multiplier;
+  B.c_force = io->contact_force; B.c_normal = io->contact_normal; B.c_point = io->contact_point;
+  B.warm_y_out = io->warm_y_out; B.warm_fix_out = io->warm_fixed_out; B.rho_out = io->rho_out;
+  B.trace_cap = io->trace_cap; B.trace_stats = io->trace_stats; B.trace_coords = io->trace_coords;
+  B.trace_c_node = io->trace_contact_node; B.trace_c_tri = io->trace_contact_triangle;
+  B.trace_c_gap = io->trace_contact_gap; B.trace_c_force = io->trace_contact_force;
+  B.trace_c_point = io->trace_contact_point;
+  if (B.trace_c_node && !(B.trace_c_tri && B.trace_c_gap && B.trace_c_force && B.trace_c_point))
+    return fail(h, ACCFEM_E_ARG, "trace contact buffers must be given together");
+  B.max_frames = io->max_frames; B.stop_on_tol = io->stop_on_tol; B.tol = io->tol;
+  B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
+  CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
+  k_solve<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, B, h->ws.p, h->ws_stride);
+  h->launches++;
+  CUDA_OK(h, cudaGetLastError());
+  return 0;
+}
+
+extern "C" int accfem_element_pass(accfem_handle* h, int32_t S, const double* x, double* f_int, double* k_diag,
+                                   double* k_off, double* frames, int32_t* degenerate, void* stream) {
+  if (!h || !x || !f_int) return ACCFEM_E_ARG;
+  if (S <= 0) return 0;
+  CUDA_OK(h, cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  long blocks = grid_blocks(h, S);
+  if (int rc = ensure_ws(h, blocks * kWarpsPerBlock, h->cmax)) return rc;
+  CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
+  k_element_pass<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, S, x, f_int, k_diag, k_off, frames,
+                                                                     degenerate, h->ws.p, h->ws_stride, h->counter.p);
+  h->launches++;
+  CUDA_OK(h, cudaGetLastError());
+  return 0;
+}
+
+extern "C" int accfem_detect(accfem_handle* h, int32_t S, const double* x, int32_t* tri, double* gap, double* point,
+                             void* stream) {
+  if (!h || !x || !tri || !gap || !point) return ACCFEM_E_ARG;
+  if (h->P.mesh.T == 0) return fail(h, ACCFEM_E_MESH, "contact detection needs a non-empty mesh");
+  if (S <= 0) return 0;
+  CUDA_OK(h, cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  long blocks = grid_blocks(h, S);
+  if (int rc = ensure_ws(h, blocks * kWarpsPerBlock, h->cmax)) return rc;
+  CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
+  k_detect<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, S, x, tri, gap, point, h->ws.p, h->ws_stride,
+                                                               h->counter.p);
+  h->launches++;
+  CUDA_OK(h, cudaGetLastError());
+  return 0;
+}
+
+// Host-pointer variant: stage inputs into handle-owned device buffers, solve,
+// copy results back.  This is the path the e2e measurement exercises.
+extern "C" int accfem_solve_batch_host(accfem_handle* h, const accfem_batch* io, void* stream) {
+  if (!h || !io) return ACCFEM_E_ARG;
+  if (io->S <= 0) return 0;
+  CUDA_OK(h, cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const long S = io->S, N = h->N, n = 6 * N, nf = h->n_fixed, nc = h->n_cables;
+  accfem_batch d = *io;
+  auto stage = [&](DevBuf<double>& b, const double* src, long cnt, const double** dst) -> int {
+    if (!src) {
+      *dst = nullptr;
+      return 0;
+    }
+    CUDA_OK(h, b.alloc(cnt));
+    CUDA_OK(h, cudaMemcpyAsync(b.p, src, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+    *dst = b.p;
+    return 0;
+  };
+  int rc = 0;
+  if ((rc = stage(h->h_x0, io->x0, S * n, &d.x0))) return rc;
+  if ((rc = stage(h->h_ten, nc ? io->tensions : nullptr, S * nc, &d.tensions))) return rc;
+  if ((rc = stage(h->h_app, io->applied, S * n, &d.applied))) return rc;
+  if ((rc = stage(h->h_ins, io->insertion, S, &d.insertion))) return rc;
+  if ((rc = stage(h->h_wy, io->warm_y_in, S * N, &d.warm_y_in))) return rc;
+  if ((rc = stage(h->h_wf, io->warm_fixed_in, S * nf, &d.warm_fixed_in))) return rc;
+  if ((rc = stage(h->h_rho, io->rho_in, S, &d.rho_in))) return rc;
+  // outputs: one double slab + one int slab
+  long nd = S * n + S + S * N * 2 + S * N * 9;
+  CUDA_OK(h, h->o_coords.alloc(nd));
+  CUDA_OK(h, h->o_ints.alloc(S * 4 + S * N * 2));
+  double* p = h->o_coords.p;
+  d.coords = p; p += S * n;
+  d.residual = p; p += S;
+  d.contact_gap = p; p += S * N;
+  d.contact_multiplier = p; p += S * N;
+  d.contact_force = p; p += S * N * 3;
+  d.contact_normal = p; p += S * N * 3;
+  d.contact_point = p; p += S * N * 3;
+  int* q = h->o_ints.p;
+  d.status = q; q += S;
+  d.frames = q; q += S;
+  d.converged = q; q += S;
+  d.n_contacts = q; q += S;
+  d.contact_node = q; q += S * N;
+  d.contact_triangle = q; q += S * N;
+  if (io->warm_y_out) { CUDA_OK(h, h->o_wy.alloc(S * N)); d.warm_y_out = h->o_wy.p; }
+  if (io->warm_fixed_out) { CUDA_OK(h, h->o_wf.alloc(S * std::max(nf, 1L))); d.warm_fixed_out = h->o_wf.p; }
+  if (io->rho_out) { CUDA_OK(h, h->o_rho.alloc(S)); d.rho_out = h->o_rho.p; }
+  long tcap = io->trace_cap;
+  bool tr_stats = io->trace_stats && tcap > 0, tr_coords = io->trace_coords && tcap > 0,
+       tr_c = io->trace_contact_node && tcap > 0;
+  if (tr_stats || tr_coords || tr_c) {
+    long tn = (tr_stats ? S * tcap * ACCFEM_TRACE_STATS : 0) + (tr_coords ? S * tcap * n : 0) +
+              (tr_c ? S * tcap * N * 7 + S * tcap * N : 0);
+    CUDA_OK(h, h->o_tr.alloc(tn));
+    double* t = h->o_tr.p;
+    if (tr_stats) { d.trace_stats = t; t += S * tcap * ACCFEM_TRACE_STATS; }
+    if (tr_coords) { d.trace_coords = t; t += S * tcap * n; }
+    if (tr_c) {
+      d.trace_contact_gap = t; t += S * tcap * N;
+      d.trace_contact_force = t; t += S * tcap * N * 3;
+      d.trace_contact_point = t; t += S * tcap * N * 3;
+      int* ti = reinterpret_cast<int*>(t);
+      d.trace_contact_node = ti; ti += S * tcap * N;
+      d.trace_contact_triangle = ti;
+    }
+  }
+  if ((rc = accfem_solve_batch(h, &d, stream))) return rc;
+  auto back = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (dst && bytes) CUDA_OK(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    return 0;
+  };
+  if ((rc = back(io->coords, d.coords, S * n * 8))) return rc;
+  if ((rc = back(io->residual, d.residual, S * 8))) return rc;
+  if ((rc = back(io->status, d.status, S * 4))) return rc;
+  if ((rc = back(io->frames, d.frames, S * 4))) return rc;
+  if ((rc = back(io->converged, d.converged, S * 4))) return rc;
+  if ((rc = back(io->n_contacts, d.n_contacts, S * 4))) return rc;
+  if ((rc = back(io->contact_node, d.contact_node, S * N * 4))) return rc;
+  if ((rc = back(io->contact_triangle, d.contact_triangle, S * N * 4))) return rc;
+  if ((rc = back(io->contact_gap, d.contact_gap, S * N * 8))) return rc;
+  if ((rc = back(io->contact_multiplier, d.contact_multiplier, S * N * 8))) return rc;
+  if ((rc = back(io->contact_force, d.contact_force, S * N * 24))) return rc;
+  if ((rc = back(io->contact_normal, d.contact_normal, S * N * 24))) return rc;
+  if ((rc = back(io->contact_point, d.contact_point, S * N * 24))) return rc;
+  if (io->warm_y_out && (rc = back(io->warm_y_out, d.warm_y_out, S * N * 8))) return rc;
+  if (io->warm_fixed_out && (rc = back(io->warm_fixed_out, d.warm_fixed_out, S * nf * 8))) return rc;
+  if (io->rho_out && (rc = back(io->rho_out, d.rho_out, S * 8))) return rc;
+  if (tr_stats && (rc = back(io->trace_stats, d.trace_stats, S * tcap * ACCFEM_TRACE_STATS * 8))) return rc;
+  if (tr_coords && (rc = back(io->trace_coords, d.trace_coords, S * tcap * n * 8))) return rc;
+  if (tr_c) {
+    if ((rc = back(io->trace_contact_node, d.trace_contact_node, S * tcap * N * 4))) return rc;
+    if ((rc = back(io->trace_contact_triangle, d.trace_contact_triangle, S * tcap * N * 4))) return rc;
+    if ((rc = back(io->trace_contact_gap, d.trace_contact_gap, S * tcap * N * 8))) return rc;
+    if ((rc = back(io->trace_contact_force, d.trace_contact_force, S * tcap * N * 24))) return rc;
+    if ((rc = back(io->trace_contact_point, d.trace_contact_point, S * tcap * N * 24))) return rc;
+  }
+  CUDA_OK(h, cudaStreamSynchronize(st));
+  return 0;
+}

@@ -1,0 +1,138 @@
+// Device-side problem description and per-scenario workspace layout.
+//
+// HBM layout (all FP64 unless noted; scenario-major, node-minor):
+//   inputs   x0[S][6N], tensions[S][nc], applied[S][6N]
+//   outputs  coords[S][6N], status/frames[S] (i32), per-frame trace, contacts
+//   model    rest directors N x 9, per-element constants E x {len, offset 9,
+//            Qa 9, Qb 9}, K_local 12x12 (kernel parameter)
+//   mesh     corners T x 9, normals T x 3, AABB lo/hi T x 3, uniform grid CSR
+//   workspace one slab per resident warp (team), see Ws below
+#pragma once
+#include "team.cuh"
+
+namespace accfem {
+
+constexpr int kMaxCables = 8;
+constexpr double kRhoMin = 1e-6, kRhoMax = 1e6, kRhoEqFactor = 1e3, kBig = 1e30;  // solver.py:36-38
+constexpr double kMinChord = 1e-9;                                                 // beam.py:23
+
+struct Settings {
+  double eps_abs, eps_rel, rho, sigma, alpha, beta0;
+  double margin, radius;  // radius = max(margin + beta0, margin)   (engine.py:148-150, contact.py:65)
+  int max_iterations, check_interval, adaptive_rho, scaling_iterations, polish;
+};
+
+struct ModelDev {
+  int N;                      // nodes
+  double l0;                  // element rest length
+  const double* rest_dir;     // N x 9
+  const double* rest_len;     // E
+  const double* offsets;      // E x 9   mean0^T E0          (beam.py:97)
+  const double* rest_frames;  // E x 9   E0
+  const double* qa;           // E x 9   T0_a^T E0
+  const double* qb;           // E x 9   T0_b^T E0
+  double kl[144];             // 12 x 12 local stiffness  (beam.py:215-253)
+  int n_fixed;
+  const int* fixed_node;      // n_fixed
+  const int* fixed_dof;       // n_fixed
+  const double* fixed_inc;    // n_fixed
+  const int* fixed_row_of_dof;  // 6N: selector row index or -1
+  int n_cables;
+  double cable_off[3 * kMaxCables];
+  double cable_dir[3 * kMaxCables];
+  double axis[3];             // insertion axis (engine.py:97-99)
+  int has_uniform;
+  double uniform[3];
+};
+
+struct MeshDev {
+  int T;                      // 0 = no mesh
+  const double* corners;      // T x 9
+  const double* normals;      // T x 3
+  const double* lo;           // T x 3 triangle AABB
+  const double* hi;           // T x 3
+  const int* tri_cell_lo;     // T x 3 clamped grid cell of the AABB lo corner
+  const int* cell_start;      // ncell + 1
+  const int* cell_tris;       // CSR payload, ascending triangle id per cell
+  double origin[3];
+  double inv_h;
+  int dims[3];
+};
+
+struct Problem {
+  Settings s;
+  ModelDev m;
+  MeshDev mesh;
+};
+
+// ---------------------------------------------------------------------------
+// per-team workspace, carved from one slab of `ws_doubles(N)` doubles
+// ---------------------------------------------------------------------------
+struct Ws {
+  // element pass
+  double *R, *frames, *fe, *ke, *fint, *KD, *KU;
+  // assembly
+  double *fa, *g, *rres;
+  // contacts (indexed by node during detection, by contact after compaction)
+  double *cgap, *cpp, *cnrm;
+  int *ctri, *cnode, *crow_of_node;
+  // rows (fixed rows first, then contacts)
+  double *lo, *up, *ls, *us, *e, *rho, *as, *z, *y, *yprev, *tr, *yfull, *warm;
+  // scaled system
+  double *HD, *HU, *gs, *d, *colh, *xs, *xt, *rhs, *w, *v, *tmp;
+  // factors: ADMM (scaled) and direct / polish (unscaled)
+  double *Li, *G, *Hb, *Li2, *G2, *Hb2;
+  // solution
+  double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr;
+  int *act, *alist;
+};
+
+constexpr int kMultiRhs = 5;  // right-hand sides solved concurrently by one warp (6 lanes each)
+
+HDEV Ws ws_carve(double* base, int N, int cmax_polish, long* used = nullptr) {
+  long n = 6L * N, E = N - 1, m = 7L * N;  // rows: <= 6N selector rows + N node contacts
+  long cp = cmax_polish;
+  Ws w;
+  double* p = base;
+  long off = 0;
+  auto take = [&](long k) { double* r = p ? p + off : nullptr; off += (k + 3) & ~3L; return r; };
+  w.R = take(9L * N); w.frames = take(9 * E); w.fe = take(12 * E); w.ke = take(108 * E);
+  w.fint = take(n); w.KD = take(36L * N); w.KU = take(36 * E);
+  w.fa = take(n); w.g = take(n); w.rres = take(n);
+  w.cgap = take(N); w.cpp = take(3L * N); w.cnrm = take(3L * N);
+  w.lo = take(m); w.up = take(m); w.ls = take(m); w.us = take(m); w.e = take(m); w.rho = take(m); w.as = take(3 * m);
+  w.z = take(m); w.y = take(m); w.yprev = take(m); w.tr = take(m); w.yfull = take(m); w.warm = take(N);
+  w.HD = take(36L * N); w.HU = take(36 * E); w.gs = take(n); w.d = take(n); w.colh = take(n);
+  w.xs = take(n); w.xt = take(n); w.rhs = take(n); w.w = take(n); w.v = take(n); w.tmp = take(n);
+  w.Li = take(36L * N); w.G = take(36L * N); w.Hb = take(36L * N);
+  w.Li2 = take(36L * N); w.G2 = take(36L * N); w.Hb2 = take(36L * N);
+  w.dx = take(n); w.dxp = take(n); w.yp = take(m); w.S = take(cp * cp); w.Sy = take(cp);
+  w.Wc = take(kMultiRhs * n);
+  w.wfix = take(n);
+  w.scr = take(128);
+  double* ib = take((5L * N + m + 8) / 2 + 1);
+  int* ip = reinterpret_cast<int*>(ib);
+  w.ctri = ip; ip = ip ? ip + N : nullptr;
+  w.cnode = ip; ip = ip ? ip + N : nullptr;
+  w.crow_of_node = ip; ip = ip ? ip + N : nullptr;
+  w.act = ip; ip = ip ? ip + m : nullptr;
+  w.alist = ip;
+  if (used) *used = off;
+  return w;
+}
+
+HDEV long ws_doubles(int N, int cmax_polish) {
+  long used = 0;
+  ws_carve(nullptr, N, cmax_polish, &used);
+  return used;
+}
+
+// ---------------------------------------------------------------------------
+// frame / scenario results written by the solver
+// ---------------------------------------------------------------------------
+struct FrameStats {
+  double dx_norm, actuation_scale, max_penetration, compl_worst, residual, pri, dua;
+  int iterations, n_c, converged, retried, compl_ok;
+};
+
+}  // namespace accfem

@@ -1,0 +1,709 @@
+// The accelerated quasi-static step on one team = one scenario:
+//   rows / assembly        fixed selector rows + node contact rows (contact.py:148-178,
+//                          constraints.py:40-63, engine.py:123-134)
+//   ruiz                   modified Ruiz equilibration (solver.py:169-212)
+//   admm                   relaxed ADMM with one cached factorisation per solve
+//                          (solver.py:250-385), infeasibility test (424-446)
+//   direct                 contact-free frames (solver.py:388-421)
+//   polish                 active-set refinement (solver.py:449-528)
+//   frame / run            Engine.step / run_static incl. retry, step limit,
+//                          multiplicative rotation update, warm state
+//                          (engine.py:136-283, solver.py:781-833)
+//
+// The KKT systems are reduced to the 6x6 block-tridiagonal normal matrix
+// (SURVEY §7.1): ADMM solves (H_s + sigma I + A_s^T diag(rho) A_s) x = r;
+// the direct and polish solves eliminate the selector rows exactly and
+// handle the active contacts through a dense Schur complement.
+#pragma once
+#include "linalg.cuh"
+#include "mech.cuh"
+
+namespace accfem {
+
+enum Status {
+  ST_OK = 0, ST_DOMAIN = 1, ST_DEGENERATE = 2, ST_MESH = 3, ST_NONCONV = 4, ST_INFEASIBLE = 5,
+  ST_ENGINE_SOLVER = 6, ST_ENGINE_MAX_FRAMES = 7, ST_CAPACITY = 8, ST_LINALG = 9
+};
+
+struct QpResult {
+  double pri, dua, rho_est;  // rho_est < 0: none reported
+  int iterations, converged;
+};
+
+struct Frame {  // per-frame problem sizes
+  int nf, nc, m;
+};
+
+// ---------------------------------------------------------------------------
+// rows
+// ---------------------------------------------------------------------------
+template <class Team>
+DEV void build_rows(const Team& team, const Problem& P, const double* x, double insertion, double scale,
+                    const Frame& F, Ws& ws) {
+  const ModelDev& M = P.m;
+  PARFOR(r, F.m) {
+    if (r < F.nf) {
+      double b = M.fixed_inc[r];
+      int nd = M.fixed_node[r], dof = M.fixed_dof[r];
+      if (insertion != 0.0 && nd == 0 && dof < 3) b += M.axis[dof] * insertion;
+      b *= scale;
+      ws.lo[r] = b;
+      ws.up[r] = b;
+    } else {
+      int c = r - F.nf;
+      int nd = ws.cnode[c];
+      const double* nr = ws.cnrm + 3 * c;
+      const double* pp = ws.cpp + 3 * c;
+      const double* p = x + 6 * nd;
+      ws.lo[r] = -kBig;
+      ws.up[r] = (nr[0] * pp[0] + nr[1] * pp[1] + nr[2] * pp[2]) - (nr[0] * p[0] + nr[1] * p[1] + nr[2] * p[2]);
+    }
+  }
+  team.sync();
+}
+
+// (A v)_r with unscaled rows
+DEV double row_dot(const Problem& P, const Frame& F, const Ws& ws, int r, const double* v) {
+  if (r < F.nf) return v[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
+  int c = r - F.nf;
+  const double* nr = ws.cnrm + 3 * c;
+  const double* vv = v + 6 * ws.cnode[c];
+  return nr[0] * vv[0] + nr[1] * vv[1] + nr[2] * vv[2];
+}
+
+// (A^T y)_j with unscaled rows; y indexed by row
+DEV double col_dot(const Problem& P, const Frame& F, const Ws& ws, int j, const double* y) {
+  double acc = 0.0;
+  int fr = P.m.fixed_row_of_dof[j];
+  if (fr >= 0) acc += y[fr];
+  int k = j / 6, cc = j % 6;
+  if (cc < 3) {
+    int c = ws.crow_of_node[k];
+    if (c >= 0) acc += ws.cnrm[3 * c + cc] * y[F.nf + c];
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// modified Ruiz equilibration of [[H, A^T], [A, 0]] + cost scaling
+// (solver.py:169-212).  Produces HD/HU (scaled H), as (scaled rows), gs, d,
+// e and returns c.
+// ---------------------------------------------------------------------------
+template <class Team>
+DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
+  const int N = P.m.N, n = 6 * N, E = N - 1;
+  const int nf = F.nf, m = F.m;
+  PARFOR(i, 36 * N) ws.HD[i] = ws.KD[i];
+  PARFOR(i, 36 * E) ws.HU[i] = ws.KU[i];
+  PARFOR(j, n) {
+    ws.gs[j] = ws.g[j];
+    ws.d[j] = 1.0;
+  }
+  PARFOR(r, m) {
+    ws.e[r] = 1.0;
+    if (r < nf) {
+      ws.as[3 * r] = 1.0;
+    } else {
+      const double* nr = ws.cnrm + 3 * (r - nf);
+      ws.as[3 * r] = nr[0];
+      ws.as[3 * r + 1] = nr[1];
+      ws.as[3 * r + 2] = nr[2];
+    }
+  }
+  team.sync();
+  double c = 1.0;
+  double* dd = ws.colh;
+  double* ee = ws.tr;
+  for (int sweep = 0; sweep < P.s.scaling_iterations; ++sweep) {
+    PARFOR(j, n) {
+      int k = j / 6, cc = j % 6;
+      double mx = 0.0;
+      for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HD[36 * k + 6 * r + cc]));
+      if (k + 1 < N)
+        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * k + 6 * cc + r]));
+      if (k > 0)
+        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * (k - 1) + 6 * r + cc]));
+      int fr = P.m.fixed_row_of_dof[j];
+      if (fr >= 0) mx = fmax(mx, fabs(ws.as[3 * fr]));
+      if (cc < 3) {
+        int ct = ws.crow_of_node[k];
+        if (ct >= 0) mx = fmax(mx, fabs(ws.as[3 * (nf + ct) + cc]));
+      }
+      dd[j] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
+    }
+    PARFOR(r, m) {
+      double mx = fabs(ws.as[3 * r]);
+      if (r >= nf) mx = fmax(mx, fmax(fabs(ws.as[3 * r + 1]), fabs(ws.as[3 * r + 2])));
+      ee[r] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
+    }
+    team.sync();
+    PARFOR(i, 36 * N) {
+      int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+      ws.HD[i] *= dd[6 * k + r] * dd[6 * k + cc];
+    }
+    PARFOR(i, 36 * E) {
+      int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+      ws.HU[i] *= dd[6 * k + r] * dd[6 * (k + 1) + cc];
+    }
+    PARFOR(r, m) {
+      if (r < nf) {
+        ws.as[3 * r] *= ee[r] * dd[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
+      } else {
+        int nd = ws.cnode[r - nf];
+        for (int q = 0; q < 3; ++q) ws.as[3 * r + q] *= ee[r] * dd[6 * nd + q];
+      }
+      ws.e[r] *= ee[r];
+    }
+    PARFOR(j, n) {
+      ws.gs[j] *= dd[j];
+      ws.d[j] *= dd[j];
+    }
+    team.sync();
+    // cost normalisation: column maxima of the scaled H only
+    double csum = 0.0, gmax = 0.0;
+    PARFOR(j, n) {
+      int k = j / 6, cc = j % 6;
+      double mx = 0.0;
+      for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HD[36 * k + 6 * r + cc]));
+      if (k + 1 < N)
+        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * k + 6 * cc + r]));
+      if (k > 0)
+        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * (k - 1) + 6 * r + cc]));
+      csum += mx;
+      gmax = fmax(gmax, fabs(ws.gs[j]));
+    }
+    csum = team.sum(csum);
+    gmax = team.max(gmax);
+    double gam = 1.0 / fmax(fmax(csum / n, gmax), 1e-12);
+    PARFOR(i, 36 * N) ws.HD[i] *= gam;
+    PARFOR(i, 36 * E) ws.HU[i] *= gam;
+    PARFOR(j, n) ws.gs[j] *= gam;
+    c *= gam;
+    team.sync();
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// residual norms of the unscaled problem at (dx = d o xs, y = e o ys / c)
+// ---------------------------------------------------------------------------
+struct Residuals {
+  double pri, dua, ps, ds;
+};
+
+template <class Team>
+DEV Residuals unscaled_residuals(const Team& team, const Problem& P, const Frame& F, Ws& ws, double c,
+                                 double gnorm) {
+  const int N = P.m.N, n = 6 * N;
+  double* xu = ws.tmp;
+  PARFOR(j, n) xu[j] = ws.d[j] * ws.xs[j];
+  team.sync();
+  double pri = 0.0, ps = 0.0;
+  PARFOR(r, F.m) {
+    double ax = row_dot(P, F, ws, r, xu);
+    double zu = ws.z[r] / ws.e[r];
+    ws.yfull[r] = ws.e[r] * ws.y[r] / c;
+    pri = fmax(pri, fabs(ax - zu));
+    ps = fmax(ps, fmax(fabs(ax), fabs(zu)));
+  }
+  block_matvec(team, N, ws.KD, ws.KU, xu, ws.v);  // includes sync
+  double dua = 0.0, ds = 0.0;
+  PARFOR(j, n) {
+    double hx = ws.v[j];
+    double aty = col_dot(P, F, ws, j, ws.yfull);
+    dua = fmax(dua, fabs(hx + ws.g[j] + aty));
+    ds = fmax(ds, fmax(fabs(hx), fabs(aty)));
+  }
+  Residuals R;
+  R.pri = team.max(pri);
+  R.ps = team.max(ps);
+  R.dua = team.max(dua);
+  R.ds = fmax(team.max(ds), gnorm);
+  return R;
+}
+
+// OSQP-style primal infeasibility test on the dual increment (solver.py:424-446)
+template <class Team>
+DEV bool infeasible(const Team& team, const Problem& P, const Frame& F, Ws& ws, double c) {
+  const int n = 6 * P.m.N;
+  double nd = 0.0;
+  PARFOR(r, F.m) {
+    double v = ws.e[r] * (ws.y[r] - ws.yprev[r]) / c;
+    ws.tr[r] = v;
+    nd = fmax(nd, fabs(v));
+  }
+  nd = team.max(nd);
+  double eps = fmax(P.s.eps_abs, 1e-10);
+  if (nd <= eps) return false;
+  team.sync();
+  double sup_u = 0.0, sup_l = 0.0;
+  PARFOR(r, F.m) {
+    double v = ws.tr[r] / nd;
+    ws.tr[r] = v;
+    sup_u += ws.up[r] * fmax(v, 0.0);
+    sup_l += ws.lo[r] * fmin(v, 0.0);
+  }
+  double support = team.sum(sup_u) + team.sum(sup_l);
+  team.sync();
+  if (!(support < -eps)) return false;
+  double at = 0.0;
+  PARFOR(j, n) at = fmax(at, fabs(col_dot(P, F, ws, j, ws.tr)));
+  at = team.max(at);
+  return at <= eps;
+}
+
+// ---------------------------------------------------------------------------
+// reduced unscaled factor for the direct / polish solves: H (+ delta I on free
+// DOFs) with selector DOFs replaced by identity rows/columns -> Li2/G2/Hb2
+// ---------------------------------------------------------------------------
+template <class Team>
+DEV int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws) {
+  const int N = P.m.N, E = N - 1;
+  const int* frd = P.m.fixed_row_of_dof;
+  PARFOR(i, 36 * N) {
+    int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+    bool fr = frd[6 * k + r] >= 0, fc = frd[6 * k + cc] >= 0;
+    double v = ws.KD[i];
+    if (fr || fc) v = (r == cc) ? 1.0 : 0.0;
+    else if (r == cc) v += delta;
+    ws.HD[i] = v;
+  }
+  PARFOR(i, 36 * E) {
+    int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+    bool fr = frd[6 * k + r] >= 0, fc = frd[6 * (k + 1) + cc] >= 0;
+    ws.HU[i] = (fr || fc) ? 0.0 : ws.KU[i];
+  }
+  team.sync();
+  return block_factor(team, N, ws.HD, ws.HU, ws.Li2, ws.G2, ws.Hb2, ws.scr);
+}
+
+// full-length rhs for the eliminated system: b at selector DOFs,
+// -g - H_{:,F} b at free DOFs.  bvec (selector values by DOF) -> out
+template <class Team>
+DEV void eliminated_rhs(const Team& team, const Problem& P, const Frame& F, Ws& ws, double* out) {
+  const int N = P.m.N, n = 6 * N;
+  double* bvec = ws.w;
+  PARFOR(j, n) {
+    int fr = P.m.fixed_row_of_dof[j];
+    bvec[j] = fr >= 0 ? ws.up[fr] : 0.0;
+  }
+  team.sync();
+  block_matvec(team, N, ws.KD, ws.KU, bvec, ws.tmp);
+  PARFOR(j, n) {
+    int fr = P.m.fixed_row_of_dof[j];
+    out[j] = fr >= 0 ? ws.up[fr] : -ws.g[j] - ws.tmp[j];
+  }
+  team.sync();
+}
+
+// selector multipliers from the exact KKT rows: y_r = -((H dx)_j + g_j + (C^T y_c)_j)
+template <class Team>
+DEV void selector_multipliers(const Team& team, const Problem& P, const Frame& F, Ws& ws, const double* dx,
+                              double* yrow) {
+  block_matvec(team, P.m.N, ws.KD, ws.KU, dx, ws.tmp);
+  PARFOR(r, F.nf) {
+    int j = 6 * P.m.fixed_node[r] + P.m.fixed_dof[r];
+    double acc = ws.tmp[j] + ws.g[j];
+    int k = j / 6, cc = j % 6;
+    if (cc < 3) {
+      int c = ws.crow_of_node[k];
+      if (c >= 0) acc += ws.cnrm[3 * c + cc] * yrow[F.nf + c];
+    }
+    yrow[r] = -acc;
+  }
+  team.sync();
+}
+
+// contact-free frame: exact selector elimination + 3 refinement rounds
+// (solver.py:388-421).  Writes ws.dx and ws.yfull[0..nf).
+template <class Team>
+DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res) {
+  const int N = P.m.N, n = 6 * N;
+  if (reduced_factor(team, P, 0.0, ws) >= 0) return ST_LINALG;
+  eliminated_rhs(team, P, F, ws, ws.rhs);
+  chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.rhs, ws.dx, 1, 0);
+  team.sync();
+  for (int it = 0; it < 3; ++it) {
+    block_matvec(team, N, ws.KD, ws.KU, ws.dx, ws.tmp);
+    PARFOR(j, n) {
+      bool fx = P.m.fixed_row_of_dof[j] >= 0;
+      ws.rhs[j] = fx ? 0.0 : -ws.g[j] - ws.tmp[j];
+    }
+    team.sync();
+    chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.rhs, ws.w, 1, 0);
+    team.sync();
+    PARFOR(j, n) ws.dx[j] += ws.w[j];
+    team.sync();
+  }
+  selector_multipliers(team, P, F, ws, ws.dx, ws.yfull);
+  double dua = 0.0;
+  block_matvec(team, N, ws.KD, ws.KU, ws.dx, ws.tmp);
+  PARFOR(j, n) dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + col_dot(P, F, ws, j, ws.yfull)));
+  res.pri = 0.0;
+  res.dua = team.max(dua);
+  res.iterations = 0;
+  res.converged = 1;
+  res.rho_est = -1.0;
+  return ST_OK;
+}
+
+// dense Cholesky + solve of the na x na Schur complement (row-major, ld = na)
+template <class Team>
+DEV bool dense_chol(const Team& team, int na, double* S) {
+  for (int k = 0; k < na; ++k) {
+    double piv = S[k * na + k];
+    if (!(piv > 0.0)) return false;
+    double l = sqrt(piv);
+    team.sync();
+    PARFOR(i, na - k) {
+      int r = k + i;
+      S[r * na + k] = (r == k) ? l : S[r * na + k] / l;
+    }
+    team.sync();
+    int rem = na - k - 1;
+    PARFOR(t, rem * rem) {
+      int r = k + 1 + t / rem, cc = k + 1 + t % rem;
+      if (cc <= r) S[r * na + cc] -= S[r * na + k] * S[cc * na + k];
+    }
+    team.sync();
+  }
+  return true;
+}
+
+template <class Team>
+DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
+  for (int k = 0; k < na; ++k) {
+    team.sync();
+    double bk = b[k] / S[k * na + k];
+    team.sync();
+    if (team.rank() == 0) b[k] = bk;
+    PARFOR(i, na - k - 1) {
+      int r = k + 1 + i;
+      b[r] -= S[r * na + k] * bk;
+    }
+  }
+  for (int k = na - 1; k >= 0; --k) {
+    team.sync();
+    double bk = b[k] / S[k * na + k];
+    team.sync();
+    if (team.rank() == 0) b[k] = bk;
+    PARFOR(i, k) b[i] -= S[k * na + i] * bk;
+  }
+  team.sync();
+}
+
+// one regularised solve of [[H+dI, C^T], [C, -dI]] [x; y] = [f; h] with the
+// selector DOFs eliminated (x_F = f_F).  f is a full-length vector; h is
+// indexed by active-contact slot.  Uses the factored S.  x -> xo, y -> yo.
+template <class Team>
+DEV void schur_solve(const Team& team, const Problem& P, Ws& ws, int na, const double* f, const double* h,
+                     double* xo, double* yo) {
+  const int N = P.m.N, n = 6 * N;
+  chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, f, ws.v, 1, 0);
+  team.sync();
+  PARFOR(q, na) {
+    int c = ws.alist[q];
+    const double* nr = ws.cnrm + 3 * c;
+    const double* vv = ws.v + 6 * ws.cnode[c];
+    yo[q] = (nr[0] * vv[0] + nr[1] * vv[1] + nr[2] * vv[2]) - h[q];
+  }
+  team.sync();
+  if (na > 0) dense_solve(team, na, ws.S, yo);
+  // x = v - P^{-1} C~^T y
+  PARFOR(j, n) ws.rhs[j] = 0.0;
+  team.sync();
+  PARFOR(q, na) {
+    int c = ws.alist[q];
+    int nd = ws.cnode[c];
+    for (int a = 0; a < 3; ++a) {
+      int j = 6 * nd + a;
+      if (P.m.fixed_row_of_dof[j] < 0) ws.rhs[j] += ws.cnrm[3 * c + a] * yo[q];
+    }
+  }
+  team.sync();
+  chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.rhs, ws.w, 1, 0);
+  team.sync();
+  PARFOR(j, n) xo[j] = ws.v[j] - ws.w[j];
+  team.sync();
+}
+
+// active-set polish (solver.py:449-528).  On entry ws.dx / ws.yfull hold the
+// ADMM result (yfull unclipped); on acceptance they are replaced.
+template <class Team>
+DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
+  const int N = P.m.N, n = 6 * N, nf = F.nf, nc = F.nc;
+  const double tol_act = fmax(10.0 * P.s.eps_abs, 1e-12);
+  const double delta = 1e-9;
+  PARFOR(c, nc) {
+    int r = nf + c;
+    double yc = fmax(ws.yfull[r], 0.0);
+    double slack = ws.up[r] - row_dot(P, F, ws, r, ws.dx);
+    ws.act[c] = (yc > tol_act) || (slack < tol_act);
+  }
+  team.sync();
+  if (reduced_factor(team, P, delta, ws) >= 0) return ST_OK;  // splu failure -> no polish
+  bool found = false;
+  double* dxp = ws.dxp;
+  double* yp = ws.yp;
+  for (int round = 0; round < 6; ++round) {
+    // active contact list in row order
+    int na = 0;
+    for (int base = 0; base < nc; base += team.size()) {
+      int c = base + team.rank();
+      bool a = c < nc && ws.act[c];
+      int tot = 0;
+      int pos = team.ballot_prefix(a, &tot);
+      if (team.size() == 1) {
+        if (a) ws.alist[na] = c;
+      } else if (a) {
+        ws.alist[na + pos] = c;
+      }
+      na += tot;
+    }
+    team.sync();
+    PARFOR(q, na) ws.alist[N + ws.alist[q]] = q;
+    team.sync();
+    if (nf + na == 0) break;
+    if (na > cmax) return ST_CAPACITY;
+    // S = C~ P^{-1} C~^T + delta I, columns in batches of kMultiRhs
+    for (int q0 = 0; q0 < na; q0 += kMultiRhs) {
+      int nb = na - q0 < kMultiRhs ? na - q0 : kMultiRhs;
+      PARFOR(t, nb * n) ws.Wc[t] = 0.0;
+      team.sync();
+      PARFOR(b, nb) {
+        int c = ws.alist[q0 + b];
+        int nd = ws.cnode[c];
+        for (int a = 0; a < 3; ++a) {
+          int j = 6 * nd + a;
+          if (P.m.fixed_row_of_dof[j] < 0) ws.Wc[b * n + j] = ws.cnrm[3 * c + a];
+        }
+      }
+      team.sync();
+      chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.Wc, ws.Wc, nb, n);
+      team.sync();
+      PARFOR(t, na * nb) {
+        int p = t / nb, b = t % nb;
+        int c = ws.alist[p];
+        const double* nr = ws.cnrm + 3 * c;
+        const double* ww = ws.Wc + b * n + 6 * ws.cnode[c];
+        double v = nr[0] * ww[0] + nr[1] * ww[1] + nr[2] * ww[2];
+        if (p == q0 + b) v += delta;
+        ws.S[p * na + q0 + b] = v;
+      }
+      team.sync();
+    }
+    // symmetrise (the two triangles agree to rounding) and factor
+    PARFOR(t, na * na) {
+      int p = t / na, q = t % na;
+      if (q > p) ws.S[q * na + p] = ws.S[p * na + q];
+    }
+    team.sync();
+    if (na > 0 && !dense_chol(team, na, ws.S)) return ST_OK;
+    // first solve: f = eliminated rhs, h = b_C
+    eliminated_rhs(team, P, F, ws, ws.xt);
+    PARFOR(q, na) ws.Sy[q] = ws.up[nf + ws.alist[q]];
+    team.sync();
+    double* yact = ws.tr;  // na entries
+    schur_solve(team, P, ws, na, ws.xt, ws.Sy, dxp, yact);
+    // one refinement round against the exact KKT
+    PARFOR(j, n) ws.tmp[j] = 0.0;
+    team.sync();
+    block_matvec(team, N, ws.KD, ws.KU, dxp, ws.xt);
+    PARFOR(j, n) {
+      bool fx = P.m.fixed_row_of_dof[j] >= 0;
+      double ct = 0.0;
+      int k = j / 6, a = j % 6;
+      if (a < 3) {
+        int c = ws.crow_of_node[k];
+        if (c >= 0 && ws.act[c]) ct = ws.cnrm[3 * c + a] * yact[ws.alist[N + c]];
+      }
+      ws.xt[j] = fx ? 0.0 : -ws.g[j] - ws.xt[j] - ct;
+    }
+    PARFOR(q, na) {
+      int c = ws.alist[q];
+      ws.Sy[q] = ws.up[nf + c] - row_dot(P, F, ws, nf + c, dxp);
+    }
+    team.sync();
+    double* dyq = ws.tr + na;
+    schur_solve(team, P, ws, na, ws.xt, ws.Sy, ws.colh, dyq);
+    PARFOR(j, n) dxp[j] += ws.colh[j];
+    PARFOR(q, na) yact[q] += dyq[q];
+    team.sync();
+    // multipliers by row: selectors from the exact KKT, active contacts, 0 otherwise
+    PARFOR(c, nc) yp[nf + c] = 0.0;
+    team.sync();
+    PARFOR(q, na) yp[nf + ws.alist[q]] = yact[q];
+    team.sync();
+    selector_multipliers(team, P, F, ws, dxp, yp);
+    int neg = 0, viol = 0;
+    PARFOR(c, nc) {
+      int r = nf + c;
+      if (ws.act[c] && yp[r] < -1e-11) neg = 1;
+      if (!ws.act[c] && row_dot(P, F, ws, r, dxp) - ws.up[r] > tol_act) viol = 1;
+    }
+    neg = team.any(neg);
+    viol = team.any(viol);
+    team.sync();
+    if (!neg && !viol) {
+      found = true;
+      break;
+    }
+    PARFOR(c, nc) {
+      int r = nf + c;
+      bool a = ws.act[c];
+      if (a && yp[r] < -1e-11) a = false;
+      else if (!a && row_dot(P, F, ws, r, dxp) - ws.up[r] > tol_act) a = true;
+      ws.act[c] = a;
+    }
+    team.sync();
+  }
+  if (!found) return ST_OK;
+  // acceptance (solver.py:483-497)
+  double pri = 0.0, fin = 1.0;
+  PARFOR(r, F.m) {
+    double ax = row_dot(P, F, ws, r, dxp);
+    pri = fmax(pri, fmax(ax - ws.up[r], 0.0));
+    if (r < nf) pri = fmax(pri, fabs(ax - ws.up[r]));
+  }
+  block_matvec(team, N, ws.KD, ws.KU, dxp, ws.tmp);
+  double dua = 0.0;
+  PARFOR(j, n) {
+    dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + col_dot(P, F, ws, j, yp)));
+    if (!isfinite(dxp[j])) fin = 0.0;
+  }
+  pri = team.max(pri);
+  dua = team.max(dua);
+  fin = team.min(fin);
+  if (fin > 0.0 && pri <= fmax(res.pri, P.s.eps_abs) && dua <= fmax(res.dua, P.s.eps_abs)) {
+    PARFOR(j, n) ws.dx[j] = dxp[j];
+    PARFOR(r, F.m) ws.yfull[r] = yp[r];
+    res.pri = pri;
+    res.dua = dua;
+  }
+  team.sync();
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one QP solve (solver.py:250-385 via solve_step 717-741).  Warm start y0 is
+// taken from ws.warm (by node) and ws.wfix.  On return ws.dx, ws.yfull.
+// ---------------------------------------------------------------------------
+template <class Team>
+DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, double rho_in, int has_wfix,
+                 QpResult& res, int cmax) {
+  const Settings& S = P.s;
+  const int N = P.m.N, n = 6 * N, nf = F.nf, m = F.m;
+  if (F.nc == 0) return direct_solve(team, P, F, ws, res);
+  double gnorm = 0.0;
+  PARFOR(j, n) gnorm = fmax(gnorm, fabs(ws.g[j]));
+  gnorm = team.max(gnorm);
+  double c = ruiz(team, P, F, ws);
+  double rho_bar = fmin(fmax(rho_in, kRhoMin), kRhoMax);
+  double rho_eq = fmin(fmax(rho_bar * kRhoEqFactor, kRhoMin), kRhoMax);
+  PARFOR(r, m) {
+    ws.rho[r] = r < nf ? rho_eq : rho_bar;
+    ws.ls[r] = ws.e[r] * ws.lo[r];
+    ws.us[r] = ws.e[r] * ws.up[r];
+  }
+  team.sync();
+  // M = H_s + sigma I + A_s^T diag(rho) A_s  (into HD; HU already holds H_s off-diagonal)
+  PARFOR(i, 36 * N) {
+    int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+    double v = ws.HD[i];
+    if (r == cc) {
+      v += S.sigma;
+      int fr = P.m.fixed_row_of_dof[6 * k + r];
+      if (fr >= 0) v += ws.rho[fr] * ws.as[3 * fr] * ws.as[3 * fr];
+    }
+    if (r < 3 && cc < 3) {
+      int ct = ws.crow_of_node[k];
+      if (ct >= 0) {
+        int row = nf + ct;
+        v += ws.rho[row] * ws.as[3 * row + r] * ws.as[3 * row + cc];
+      }
+    }
+    ws.HD[i] = v;
+  }
+  team.sync();
+  if (block_factor(team, N, ws.HD, ws.HU, ws.Li, ws.G, ws.Hb, ws.scr) >= 0) return ST_LINALG;
+  // initial iterate (solver.py:287-289)
+  PARFOR(j, n) ws.xs[j] = 0.0;
+  PARFOR(r, m) {
+    double y0;
+    if (r < nf) y0 = has_wfix ? ws.wfix[r] : 0.0;
+    else y0 = ws.warm[ws.cnode[r - nf]];
+    ws.y[r] = c * y0 / ws.e[r];
+    ws.z[r] = fmin(fmax(0.0, ws.ls[r]), ws.us[r]);
+  }
+  team.sync();
+  const double al = S.alpha, sg = S.sigma;
+  double rho_est = rho_bar;
+  int k = 0;
+  bool infeas = false;
+  for (k = 1; k <= S.max_iterations; ++k) {
+    PARFOR(r, m) ws.tr[r] = ws.rho[r] * (ws.z[r] - ws.y[r] / ws.rho[r]);
+    team.sync();
+    PARFOR(j, n) {
+      double v = sg * ws.xs[j] - ws.gs[j];
+      int fr = P.m.fixed_row_of_dof[j];
+      if (fr >= 0) v += ws.as[3 * fr] * ws.tr[fr];
+      int cc = j % 6;
+      if (cc < 3) {
+        int ct = ws.crow_of_node[j / 6];
+        if (ct >= 0) v += ws.as[3 * (nf + ct) + cc] * ws.tr[nf + ct];
+      }
+      ws.rhs[j] = v;
+    }
+    team.sync();
+    chain_solve(team, N, ws.Li, ws.G, ws.Hb, ws.rhs, ws.xt, 1, 0);
+    team.sync();
+    PARFOR(r, m) {
+      double zt;
+      if (r < nf) {
+        zt = ws.as[3 * r] * ws.xt[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
+      } else {
+        const double* xx = ws.xt + 6 * ws.cnode[r - nf];
+        zt = ws.as[3 * r] * xx[0] + ws.as[3 * r + 1] * xx[1] + ws.as[3 * r + 2] * xx[2];
+      }
+      double z = ws.z[r], y = ws.y[r], rh = ws.rho[r];
+      double zr = al * zt + (1.0 - al) * z;
+      double zn = fmin(fmax(zr + y / rh, ws.ls[r]), ws.us[r]);
+      ws.yprev[r] = y;
+      ws.y[r] = y + rh * (zr - zn);
+      ws.z[r] = zn;
+    }
+    PARFOR(j, n) ws.xs[j] = al * ws.xt[j] + (1.0 - al) * ws.xs[j];
+    team.sync();
+    if (k <= 8 || k % S.check_interval == 0 || k == S.max_iterations) {
+      Residuals R = unscaled_residuals(team, P, F, ws, c, gnorm);
+      team.sync();
+      if (R.pri <= S.eps_abs + S.eps_rel * R.ps && R.dua <= S.eps_abs + S.eps_rel * R.ds) break;
+      if (k % S.check_interval == 0) {
+        infeas = infeasible(team, P, F, ws, c);
+        team.sync();
+        if (infeas) break;
+        if (k == S.check_interval) {
+          double ratio = (R.pri / fmax(R.ps, 1e-12)) / fmax(R.dua / fmax(R.ds, 1e-12), 1e-12);
+          rho_est = fmin(fmax(rho_bar * sqrt(ratio), kRhoMin), kRhoMax);
+        }
+      }
+    }
+  }
+  if (k > S.max_iterations) k = S.max_iterations;
+  if (infeas) return ST_INFEASIBLE;
+  Residuals R = unscaled_residuals(team, P, F, ws, c, gnorm);
+  PARFOR(j, n) ws.dx[j] = ws.tmp[j];  // tmp holds d o xs
+  team.sync();
+  res.pri = R.pri;
+  res.dua = R.dua;
+  res.iterations = k;
+  res.converged = (R.pri <= S.eps_abs + S.eps_rel * R.ps && R.dua <= S.eps_abs + S.eps_rel * R.ds) ? 1 : 0;
+  res.rho_est = (S.adaptive_rho && k >= 3 * S.check_interval) ? rho_est : -1.0;
+  if (S.polish && res.converged) {
+    int st = polish(team, P, F, ws, res, cmax);
+    if (st != ST_OK) return st;
+  }
+  return res.converged ? ST_OK : ST_NONCONV;
+}
+
+}  // namespace accfem

@@ -1,0 +1,113 @@
+// Execution "team" abstraction shared by the device build (nvcc, sm_100a)
+// and the serial test-only emulation build (g++).
+//
+// Device: one warp = one team = one scenario.  PARFOR strides the lanes,
+// team.sync() is __syncwarp (which also orders the warp's memory traffic),
+// reductions are butterfly shuffles so every lane ends with the result.
+// Emulation: one "lane" runs every PARFOR iteration in order.
+#pragma once
+
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define DEV __device__ __forceinline__
+#define DEVNI __device__ __noinline__
+#define HDEV __host__ __device__ inline
+#else
+#include <math.h>
+#include <string.h>
+#include <algorithm>
+#define DEV inline
+#define DEVNI inline
+#define HDEV inline
+#endif
+
+#define PARFOR(i, n) for (int i = team.rank(); i < (n); i += team.size())
+
+namespace accfem {
+
+#if defined(__CUDACC__)
+struct TeamWarp {
+  int lane;
+  DEV int rank() const { return lane; }
+  DEV int size() const { return 32; }
+  DEV void sync() const { __syncwarp(); }
+  DEV double max(double v) const {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  }
+  DEV double min(double v) const {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  }
+  DEV double sum(double v) const {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  }
+  DEV int isum(int v) const {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  }
+  DEV int imin(int v) const {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = ::min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  }
+  DEV int any(bool p) const { return __any_sync(0xffffffffu, p); }
+  DEV double bcast(double v, int src) const { return __shfl_sync(0xffffffffu, v, src); }
+  DEV int ibcast(int v, int src) const { return __shfl_sync(0xffffffffu, v, src); }
+  // exclusive prefix over flags in lane order within one 32-wide chunk
+  DEV int ballot_prefix(bool p, int* total) const {
+    unsigned b = __ballot_sync(0xffffffffu, p);
+    *total = __popc(b);
+    return __popc(b & ((1u << lane) - 1u));
+  }
+};
+#endif
+
+struct TeamSerial {
+  DEV int rank() const { return 0; }
+  DEV int size() const { return 1; }
+  DEV void sync() const {}
+  DEV double max(double v) const { return v; }
+  DEV double min(double v) const { return v; }
+  DEV double sum(double v) const { return v; }
+  DEV int isum(int v) const { return v; }
+  DEV int imin(int v) const { return v; }
+  DEV int any(bool p) const { return p; }
+  DEV double bcast(double v, int) const { return v; }
+  DEV int ibcast(int v, int) const { return v; }
+  DEV int ballot_prefix(bool p, int* total) const {
+    *total = p ? 1 : 0;
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// IEEE round-to-nearest arithmetic with no FMA contraction: the narrow phase
+// must reproduce numpy's operation order bit for bit.
+// ---------------------------------------------------------------------------
+#if defined(__CUDA_ARCH__)
+DEV double xmul(double a, double b) { return __dmul_rn(a, b); }
+DEV double xadd(double a, double b) { return __dadd_rn(a, b); }
+DEV double xsub(double a, double b) { return __dsub_rn(a, b); }
+#else
+DEV double xmul(double a, double b) { return a * b; }
+DEV double xadd(double a, double b) { return a + b; }
+DEV double xsub(double a, double b) { return a - b; }
+#endif
+
+// numpy einsum("ij,ij->i") over 3 columns sums (0, 2) first, then 1
+DEV double edot3(const double* a, const double* b) {
+  return xadd(xadd(xmul(a[0], b[0]), xmul(a[2], b[2])), xmul(a[1], b[1]));
+}
+// numpy linalg.norm(axis=1) over 3 columns: sqrt((x0^2 + x1^2) + x2^2)
+DEV double enorm3(const double* a) {
+  return sqrt(xadd(xadd(xmul(a[0], a[0]), xmul(a[1], a[1])), xmul(a[2], a[2])));
+}
+
+}  // namespace accfem

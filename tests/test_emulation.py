@@ -1,0 +1,92 @@
+"""CPU check of the DEVICE algorithm: the team-generic CUDA source compiled
+with g++ (tests/emu, test-only) against the reference goldens.  Same bars as
+the GPU parity suite."""
+
+import numpy as np
+import pytest
+
+from paper_2503_06922_b200 import scenarios
+from paper_2503_06922_b200.scene import FixedNodeSpec, MaterialParams, TriangleMesh, straight_model
+
+from emu.emu_binding import EmuEngine
+
+
+def emu_solve(w):
+    e = EmuEngine(**w.engine_kwargs())
+    H = e.solve(w.x0, w.tensions, w.applied, w.tol, w.max_frames, trace_cap=w.max_frames)
+    return H
+
+
+def check(g, tag, H, i):
+    assert H["status"][i] == int(g[f"{tag}_status"]), tag
+    assert H["frames"][i] == int(g[f"{tag}_frames"]), tag
+    its = H["trace_stats"][i, :H["frames"][i], 5].astype(np.int32)
+    assert np.array_equal(its, g[f"{tag}_iterations"]), tag
+    nc = H["n_contacts"][i]
+    assert np.array_equal(H["contact_node"][i, :nc], g[f"{tag}_contact_nodes"])
+    assert np.array_equal(H["contact_triangle"][i, :nc], g[f"{tag}_contact_tris"])
+    ref = g[f"{tag}_coords"]
+    assert np.abs(H["coords"][i] - ref).max() <= 1e-6 * np.abs(ref).max()
+    fr = g[f"{tag}_contact_forces"]
+    if fr.size:
+        assert np.abs(H["contact_force"][i, :nc] - fr).max() <= 1e-5 * np.abs(fr).max()
+    frame_res = g[f"{tag}_frame_residual"]
+    got_res = H["trace_stats"][i, :H["frames"][i], 4]
+    assert np.allclose(got_res, frame_res, rtol=1e-5, atol=1e-9)
+    assert np.allclose(H["trace_stats"][i, :H["frames"][i], 1], g[f"{tag}_frame_scale"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg5"])
+def test_emulated_solves_match_reference(golden, name):
+    g = golden("solves.npz")
+    w = scenarios.cfg1(3, seed=1) if name == "cfg1" else scenarios.CONFIGS[name](1)
+    H = emu_solve(w)
+    for i in range(w.size):
+        check(g, f"{name}_{i}", H, i)
+
+
+def test_emulated_cfg2_and_cfg4_match_reference(golden):
+    g = golden("solves.npz")
+    H = emu_solve(scenarios.cfg2(1))
+    check(g, "cfg2_0", H, 0)
+    w = scenarios.cfg4(16)
+    H = emu_solve(w)
+    for i in range(16):
+        check(g, f"cfg4_{i}", H, i)
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_emulated_element_pass(golden, tag):
+    g = golden("beam.npz")
+    model = straight_model(int(g[f"{tag}_nodes"]), float(g[f"{tag}_length"]),
+                           MaterialParams(510e6, 5.551e-6, 5.041e-12))
+    e = EmuEngine(model, fixed_specs=[FixedNodeSpec(0)], settings=scenarios.SolverSettings())
+    f, kd, ku, bad = e.element_pass(g[f"{tag}_coords"])
+    assert not bad.any()
+    for i in range(len(f)):
+        scale = np.abs(g[f"{tag}_kd"][i]).max()
+        assert np.abs(f[i] - g[f"{tag}_fint"][i]).max() <= 1e-9 * max(np.abs(g[f"{tag}_fint"][i]).max(), 1e-3)
+        assert np.abs(kd[i] - g[f"{tag}_kd"][i]).max() <= 1e-12 * scale
+        assert np.abs(ku[i] - g[f"{tag}_ku"][i]).max() <= 1e-12 * scale
+
+
+def test_emulated_detection_bit_exact(golden):
+    g = golden("detect.npz")
+    model = straight_model(12, 0.55, MaterialParams(510e6, 5.551e-6, 5.041e-12))
+    verts, counts, ref = g["rand_verts"], g["rand_tri_counts"], g["rand_contacts"]
+    start = 0
+    for s, n_tri in enumerate(counts):
+        v = verts[start:start + 3 * n_tri]
+        start += 3 * n_tri
+        mesh = TriangleMesh(v, np.arange(3 * n_tri).reshape(-1, 3))
+        m = float(g["rand_margins"][s])
+        e = EmuEngine(model, mesh=mesh, fixed_specs=[FixedNodeSpec(0)], margin=m,
+                      settings=scenarios.SolverSettings(beta0=1e-300))
+        coords = model.rest_configuration.reshape(-1, 6).copy()
+        coords[:, :3] = g["rand_positions"][s]
+        tri, gap, pt = e.detect(coords.reshape(1, -1))
+        want = ref[ref[:, 0] == s]
+        nodes = np.flatnonzero(tri[0] >= 0)
+        assert np.array_equal(nodes, want[:, 1].astype(int)), s
+        for k, r in zip(nodes, want):
+            assert tri[0, k] == int(r[2]) and gap[0, k] == r[3] and np.array_equal(pt[0, k], r[4:7])

@@ -1,0 +1,219 @@
+"""Device parity: the sm_100a library through the C ABI vs the reference's
+golden fixtures and the CPU oracle.  Bars (BASELINE.json north_star):
+coords <= 1e-6 relative, contact forces <= 1e-5 relative, contact sets
+identical, frame counts and per-frame ADMM iteration counts equal, status
+equal.  Bit-exact for the detection narrow phase."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import accfem_oracle as O  # noqa: E402
+from paper_2503_06922_b200 import scenarios  # noqa: E402
+from paper_2503_06922_b200.scene import (  # noqa: E402
+    Configuration,
+    FixedNodeSpec,
+    MaterialParams,
+    SolverSettings,
+    StepInputs,
+    TriangleMesh,
+    make_rectangle,
+    straight_model,
+)
+
+DEV = "cuda:0"
+COORD_TOL = 1e-6
+FORCE_TOL = 1e-5
+
+
+def engine_for(w, **kw):
+    from paper_2503_06922_b200.engine import Engine
+    return Engine(**w.engine_kwargs(), device=0, **kw)
+
+
+def device_solve(w, host=False):
+    eng = engine_for(w)
+    if host:
+        res = eng.solve_static_batch(w.x0, w.tensions, w.applied, tol=w.tol, max_frames=w.max_frames)
+        return res, eng
+    t = lambda a: None if a is None else torch.tensor(a, device=DEV)  # noqa: E731
+    res = eng.solve_static_batch(t(w.x0), t(w.tensions), t(w.applied), tol=w.tol, max_frames=w.max_frames)
+    torch.cuda.synchronize()
+    return res.to_numpy(), eng
+
+
+def check_against_golden(g, tag, r, i):
+    assert int(r.status[i]) == int(g[f"{tag}_status"]), tag
+    if int(r.status[i]) != 0:
+        return
+    assert int(r.frames[i]) == int(g[f"{tag}_frames"]), tag
+    nc = int(r.n_contacts[i])
+    assert np.array_equal(r.contact_node[i, :nc], g[f"{tag}_contact_nodes"]), tag
+    assert np.array_equal(r.contact_triangle[i, :nc], g[f"{tag}_contact_tris"]), tag
+    ref = g[f"{tag}_coords"]
+    assert np.abs(r.coords[i] - ref).max() <= COORD_TOL * np.abs(ref).max(), tag
+    fr = g[f"{tag}_contact_forces"]
+    if fr.size:
+        assert np.abs(r.contact_force[i, :nc] - fr).max() <= FORCE_TOL * np.abs(fr).max(), tag
+    assert abs(float(r.residual[i]) - float(g[f"{tag}_residual"])) <= 1e-6 * max(1.0, float(g[f"{tag}_residual"]))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg2", "cfg5"])
+def test_static_solves_match_reference_goldens(golden, name):
+    g = golden("solves.npz")
+    w = scenarios.cfg1(3, seed=1) if name == "cfg1" else scenarios.CONFIGS[name](1)
+    r, _ = device_solve(w)
+    for i in range(w.size):
+        check_against_golden(g, f"{name}_{i}", r, i)
+
+
+def test_cfg4_batch_matches_reference_goldens(golden):
+    g = golden("solves.npz")
+    w = scenarios.cfg4(16)
+    r, _ = device_solve(w)
+    for i in range(16):
+        check_against_golden(g, f"cfg4_{i}", r, i)
+
+
+def test_cfg4_batch_matches_oracle_and_host_path():
+    w = scenarios.cfg4(48, start=100)
+    r, _ = device_solve(w)
+    rh, _ = device_solve(w, host=True)
+    ref = O.solve_workload(w, indices=range(0, 48, 6))
+    for j, i in enumerate(range(0, 48, 6)):
+        o = ref[j]
+        assert int(r.status[i]) == o["status"]
+        assert int(r.frames[i]) == o["frames"]
+        nc = int(r.n_contacts[i])
+        assert np.array_equal(r.contact_node[i, :nc], o["contact_nodes"])
+        assert np.array_equal(r.contact_triangle[i, :nc], o["contact_tris"])
+        assert np.abs(r.coords[i] - o["coords"]).max() <= COORD_TOL * np.abs(o["coords"]).max()
+    # host-buffer C ABI path is the same computation
+    assert np.array_equal(rh.coords, r.coords)
+    assert np.array_equal(rh.frames, r.frames)
+
+
+def test_run_static_records_match_oracle_iteration_counts():
+    from paper_2503_06922_b200.engine import Engine
+    w = scenarios.cfg3(1)
+    eng = Engine(**w.engine_kwargs(), device=0)
+    x, recs, resid = eng.run_static(StepInputs(tensions=w.tensions[0], applied_force=w.applied[0]),
+                                    x0=Configuration(w.x0[0].copy()), tol=w.tol, max_frames=w.max_frames)
+    oe = O.OracleEngine(**w.engine_kwargs())
+    ox, orecs = oe.run_static(w.x0[0], w.tensions[0], w.applied[0], tol=w.tol, max_frames=w.max_frames)
+    assert [r.iterations for r in recs] == [r.iterations for r in orecs]
+    assert [r.n_c for r in recs] == [r.n_c for r in orecs]
+    for a, b in zip(recs, orecs):
+        assert a.complementarity_ok == b.compl_ok
+        assert a.retried == b.retried
+        assert abs(a.actuation_scale - b.actuation_scale) <= 1e-9
+        assert abs(a.dx_norm - b.dx_norm) <= 1e-6 * max(b.dx_norm, 1e-9)
+        assert abs(a.residual_norm - b.residual) <= 1e-6 * max(1.0, b.residual)
+        assert [c.triangle_id for c in a.contact_points] == [c[1] for c in b.contacts]
+    assert np.abs(x.coords - ox).max() <= COORD_TOL * np.abs(ox).max()
+    # engine state persists: a second run_static from the solution converges at once
+    x2, recs2, _ = eng.run_static(StepInputs(tensions=w.tensions[0], applied_force=w.applied[0]), x0=x, tol=1e-6)
+    assert len(recs2) >= 1
+
+
+def test_step_matches_oracle_frame():
+    from paper_2503_06922_b200.engine import Engine
+    w = scenarios.cfg3p(1)
+    eng = Engine(**w.engine_kwargs(), device=0)
+    oe = O.OracleEngine(**w.engine_kwargs())
+    x = Configuration(w.x0[0].copy())
+    ox = w.x0[0].copy()
+    for k in range(3):
+        x, rec = eng.step(x, StepInputs(applied_force=w.applied[0]), frame_index=k)
+        fr = oe.step(ox, None, w.applied[0])
+        ox = fr.coords
+        assert rec.iterations == fr.iterations
+        assert rec.n_c == fr.n_c
+        assert np.abs(x.coords - ox).max() <= 1e-9 * np.abs(ox).max()
+        assert np.abs(rec.contact_force_vectors - fr.forces).max() <= FORCE_TOL * np.abs(fr.forces).max()
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_element_pass_matches_reference(golden, tag):
+    from paper_2503_06922_b200.engine import Engine
+    g = golden("beam.npz")
+    model = straight_model(int(g[f"{tag}_nodes"]), float(g[f"{tag}_length"]),
+                           MaterialParams(510e6, 5.551e-6, 5.041e-12))
+    eng = Engine(model, fixed_specs=[FixedNodeSpec(0)], device=0)
+    f, kd, ku, _, bad = eng.element_pass(torch.tensor(g[f"{tag}_coords"], device=DEV))
+    f, kd, ku = f.cpu().numpy(), kd.cpu().numpy(), ku.cpu().numpy()
+    assert not bad.any()
+    for i in range(len(f)):
+        scale = np.abs(g[f"{tag}_kd"][i]).max()
+        assert np.abs(f[i] - g[f"{tag}_fint"][i]).max() <= 1e-9 * max(np.abs(g[f"{tag}_fint"][i]).max(), 1e-3)
+        assert np.abs(kd[i] - g[f"{tag}_kd"][i]).max() <= 1e-12 * scale
+        assert np.abs(ku[i] - g[f"{tag}_ku"][i]).max() <= 1e-12 * scale
+
+
+def test_detection_bit_exact_on_random_soups(golden):
+    """test_contact.py:113-130 recipe (seed 42): gap and plane_point bit-exact."""
+    from paper_2503_06922_b200.engine import Engine
+    g = golden("detect.npz")
+    model = straight_model(12, 0.55, MaterialParams(510e6, 5.551e-6, 5.041e-12))
+    verts, counts, ref = g["rand_verts"], g["rand_tri_counts"], g["rand_contacts"]
+    start = 0
+    for s, n_tri in enumerate(counts):
+        v = verts[start:start + 3 * n_tri]
+        start += 3 * n_tri
+        mesh = TriangleMesh(v, np.arange(3 * n_tri).reshape(-1, 3))
+        m = float(g["rand_margins"][s])
+        # detect_contacts(x, model, mesh, margin) with query radius = margin
+        eng = Engine(model, mesh=mesh, fixed_specs=[FixedNodeSpec(0)], margin=m,
+                     settings=SolverSettings(beta0=1e-300), device=0)
+        coords = model.rest_configuration.reshape(-1, 6).copy()
+        coords[:, :3] = g["rand_positions"][s]
+        tri, gap, pt = eng.detect(torch.tensor(coords.reshape(1, -1), device=DEV))
+        tri, gap, pt = tri.cpu().numpy()[0], gap.cpu().numpy()[0], pt.cpu().numpy()[0]
+        want = ref[ref[:, 0] == s]
+        got_nodes = np.flatnonzero(tri >= 0)
+        assert np.array_equal(got_nodes, want[:, 1].astype(int)), s
+        for k, r in zip(got_nodes, want):
+            assert tri[k] == int(r[2])
+            assert gap[k] == r[3]
+            assert np.array_equal(pt[k], r[4:7])
+
+
+def test_detection_matches_oracle_on_lumen_states():
+    w = scenarios.cfg3(1)
+    eng = engine_for(w)
+    lum = O.Lumen(w.mesh)
+    rng = np.random.default_rng(5)
+    xs = np.tile(w.x0[0], (64, 1))
+    xs.reshape(64, -1, 6)[:, :, :3] += rng.normal(size=(64, w.model.node_count, 3)) * 2e-4
+    tri, gap, pt = (a.cpu().numpy() for a in eng.detect(torch.tensor(xs, device=DEV)))
+    for s in range(64):
+        cs = O.detect(lum, xs[s].reshape(-1, 6)[:, :3], w.margin, w.margin + w.settings.beta0)
+        assert [c[0] for c in cs] == list(np.flatnonzero(tri[s] >= 0))
+        for c in cs:
+            assert tri[s, c[0]] == c[1] and gap[s, c[0]] == c[2] and np.array_equal(pt[s, c[0]], c[3])
+
+
+def test_degenerate_element_status():
+    w = scenarios.cfg1(1)
+    x0 = w.x0.copy()
+    x0[0, 6:9] = x0[0, 0:3]  # nodes 0 and 1 coincide
+    w.x0 = x0
+    r, _ = device_solve(w)
+    assert int(r.status[0]) == 2  # DegenerateElementError
+
+
+def test_max_frames_status():
+    w = scenarios.cfg3(1)
+    w.max_frames = 3
+    r, _ = device_solve(w)
+    assert int(r.status[0]) == 7  # EngineError (static mode did not converge)
+
+
+def test_empty_batch_and_launch_count():
+    w = scenarios.cfg3p(1)
+    eng = engine_for(w)
+    before = eng.launches
+    out = eng.solve_static_batch(torch.zeros((0, w.model.dof_count), dtype=torch.float64, device=DEV))
+    assert eng.launches == before and out.coords.shape[0] == 0
