@@ -22,20 +22,27 @@ def stale():
     return os.path.getmtime(SO) < max(os.path.getmtime(p) for p in sources())
 
 
-def build(force=False, verbose=False):
-    """Compile csrc/accfem.cu -> libaccfem.so when any source is newer."""
-    if not force and not stale():
-        return SO
-    cmd = [NVCC, *FLAGS, "-o", SO + ".tmp", os.path.join(CSRC, "accfem.cu"), "-lcudart"]
+def build(force=False, verbose=False, profile=False):
+    """Compile csrc/accfem.cu -> libaccfem.so when any source is newer.
+
+    profile=True builds the development variant libaccfem_prof.so with the
+    per-phase clock counters (-DACCFEM_PROFILE); the package never loads it.
+    """
+    so = SO.replace(".so", "_prof.so") if profile else SO
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= max(os.path.getmtime(p) for p in sources()):
+        return so
+    extra = ["-DACCFEM_PROFILE"] if profile else []
+    cmd = [NVCC, *FLAGS, *extra, "-o", so + ".tmp", os.path.join(CSRC, "accfem.cu"), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(res.stderr)
-    os.replace(SO + ".tmp", SO)
+    if not profile:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+            fh.write(res.stderr)
+    os.replace(so + ".tmp", so)
     if verbose:
         print(res.stderr)
-    return SO
+    return so
 
 
 if __name__ == "__main__":

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_solve(Problem P, BatchD
   TeamWarp team{(int)(threadIdx.x & 31)};
   const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, B.cmax_polish);
+  ws.prof = B.prof ? B.prof + wid * PF_COUNT : nullptr;
   while (true) {
     int s = 0;
     if (team.lane == 0) s = atomicAdd(B.work_counter, 1);
@@ -142,7 +143,20 @@ struct accfem_handle {
   // host-path staging (accfem_solve_batch_host)
   DevBuf<double> h_x0, h_ten, h_app, h_ins, h_wy, h_wf, h_rho, o_coords, o_res, o_cd, o_wy, o_wf, o_rho, o_tr;
   DevBuf<int> o_ints;
+  unsigned long long* prof = nullptr;  // development: per-team phase counters
 };
+
+// development hook (not part of include/accfem.h): per-team phase clock
+// counters, PF_COUNT per resident team, in builds with -DACCFEM_PROFILE
+extern "C" int accfem_dev_set_profile(accfem_handle* h, void* counters) {
+  if (!h) return ACCFEM_E_ARG;
+  h->prof = (unsigned long long*)counters;
+#if defined(ACCFEM_PROFILE)
+  return 0;
+#else
+  return 1;
+#endif
+}
 
 static int fail(accfem_handle* h, int code, const std::string& msg) {
   if (h) h->err = msg;
@@ -358,6 +372,7 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
     return fail(h, ACCFEM_E_ARG, "trace contact buffers must be given together");
   B.max_frames = io->max_frames; B.stop_on_tol = io->stop_on_tol; B.tol = io->tol;
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
+  B.prof = h->prof;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
   k_solve<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, B, h->ws.p, h->ws_stride);
   h->launches++;

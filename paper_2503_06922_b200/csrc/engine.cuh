@@ -44,6 +44,7 @@ struct BatchDev {
   int fail_on_limit;         // 1: exhausting max_frames is ST_ENGINE_MAX_FRAMES
   int cmax_polish;
   int* work_counter;         // dynamic scenario queue
+  unsigned long long* prof;  // per-team phase counters (profile builds)
 };
 
 constexpr int kTraceStats = 12;  // dx_norm, act_scale, max_pen, compl_worst, residual, iterations,
@@ -56,7 +57,9 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
                    bool& pending, double& resid_prev, FrameStats& st, Frame& F) {
   const ModelDev& M = P.m;
   const int N = M.N, n = 6 * N;
+  PROF_T0(t_el);
   int bad = element_pass(team, P, x, ws, true);
+  PROF_ADD(ws, PF_ELEMENT, t_el);
   if (bad) return ST_DEGENERATE;
   if (pending) {
     double acc = 0.0;
@@ -68,7 +71,9 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
     pending = false;
   }
   F.nf = M.n_fixed;
+  PROF_T0(t_det);
   F.nc = P.mesh.T > 0 ? detect_pass(team, P, x, ws) : 0;
+  PROF_ADD(ws, PF_DETECT, t_det);
   if (P.mesh.T == 0) {
     PARFOR(k, N) ws.crow_of_node[k] = -1;
     team.sync();
@@ -88,6 +93,7 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
   }
   if (code != ST_OK) return code;
   const int nf = F.nf, nc = F.nc;
+  PROF_T0(t_post);
   // complementarity report on the unlimited result (solver.py:781-800)
   double mult_v = 0.0, gap_v = 0.0, prod_v = 0.0, eq_v = 0.0, ymax = 0.0, axmax = 0.0, nrm2 = 0.0;
   PARFOR(r, F.m) {
@@ -157,6 +163,7 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
   PARFOR(j, n) ws.rres[j] = col_dot(P, F, ws, j, ws.yp) - ws.fa[j];
   team.sync();
   pending = true;
+  PROF_ADD(ws, PF_POST, t_post);
   st.dx_norm = sqrt(team.sum(dxn2));
   st.actuation_scale = fac;
   st.max_penetration = fmax(fmax(team.max(pen0), 0.0), fmax(team.max(pen1), 0.0));
@@ -233,6 +240,7 @@ DEV void run_scenario(const Team& team, const Problem& P, const BatchDev& B, int
   F.nf = M.n_fixed;
   F.nc = 0;
   F.m = F.nf;
+  PROF_T0(t_tot);
   for (f = 0; f < B.max_frames; ++f) {
     FrameStats cur;
     double resid_prev = 0.0;
@@ -262,6 +270,10 @@ DEV void run_scenario(const Team& team, const Problem& P, const BatchDev& B, int
     }
   }
   int frames_done = f;
+  PROF_ADD(ws, PF_TOTAL, t_tot);
+#if defined(__CUDA_ARCH__) && defined(ACCFEM_PROFILE)
+  if (ws.prof && team.rank() == 0) ws.prof[PF_FRAMES] += frames_done;
+#endif
   if (status == ST_OK) {
     // last frame: contacts, and its residual from one more F_int pass
     long o = (long)s * N;

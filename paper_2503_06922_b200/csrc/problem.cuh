@@ -85,6 +85,7 @@ struct Ws {
   // solution
   double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr;
   int *act, *alist;
+  unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
 };
 
 constexpr int kMultiRhs = 5;  // right-hand sides solved concurrently by one warp (6 lanes each)
@@ -117,6 +118,7 @@ HDEV Ws ws_carve(double* base, int N, int cmax_polish, long* used = nullptr) {
   w.crow_of_node = ip; ip = ip ? ip + N : nullptr;
   w.act = ip; ip = ip ? ip + m : nullptr;
   w.alist = ip;
+  w.prof = nullptr;
   if (used) *used = off;
   return w;
 }

@@ -593,11 +593,18 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
                  QpResult& res, int cmax) {
   const Settings& S = P.s;
   const int N = P.m.N, n = 6 * N, nf = F.nf, m = F.m;
-  if (F.nc == 0) return direct_solve(team, P, F, ws, res);
+  if (F.nc == 0) {
+    PROF_T0(t_dir);
+    int st = direct_solve(team, P, F, ws, res);
+    PROF_ADD(ws, PF_DIRECT, t_dir);
+    return st;
+  }
   double gnorm = 0.0;
   PARFOR(j, n) gnorm = fmax(gnorm, fabs(ws.g[j]));
   gnorm = team.max(gnorm);
+  PROF_T0(t_ruiz);
   double c = ruiz(team, P, F, ws);
+  PROF_ADD(ws, PF_RUIZ, t_ruiz);
   double rho_bar = fmin(fmax(rho_in, kRhoMin), kRhoMax);
   double rho_eq = fmin(fmax(rho_bar * kRhoEqFactor, kRhoMin), kRhoMax);
   PARFOR(r, m) {
@@ -625,7 +632,10 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     ws.HD[i] = v;
   }
   team.sync();
-  if (block_factor(team, N, ws.HD, ws.HU, ws.Li, ws.G, ws.Hb, ws.scr) >= 0) return ST_LINALG;
+  PROF_T0(t_fac);
+  int fbad = block_factor(team, N, ws.HD, ws.HU, ws.Li, ws.G, ws.Hb, ws.scr);
+  PROF_ADD(ws, PF_FACTOR, t_fac);
+  if (fbad >= 0) return ST_LINALG;
   // initial iterate (solver.py:287-289)
   PARFOR(j, n) ws.xs[j] = 0.0;
   PARFOR(r, m) {
@@ -640,6 +650,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   double rho_est = rho_bar;
   int k = 0;
   bool infeas = false;
+  PROF_T0(t_iter);
   for (k = 1; k <= S.max_iterations; ++k) {
     PARFOR(r, m) ws.tr[r] = ws.rho[r] * (ws.z[r] - ws.y[r] / ws.rho[r]);
     team.sync();
@@ -655,8 +666,10 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
       ws.rhs[j] = v;
     }
     team.sync();
+    PROF_T0(t_ch);
     chain_solve(team, N, ws.Li, ws.G, ws.Hb, ws.rhs, ws.xt, 1, 0);
     team.sync();
+    PROF_ADD(ws, PF_CHAIN, t_ch);
     PARFOR(r, m) {
       double zt;
       if (r < nf) {
@@ -675,8 +688,10 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     PARFOR(j, n) ws.xs[j] = al * ws.xt[j] + (1.0 - al) * ws.xs[j];
     team.sync();
     if (k <= 8 || k % S.check_interval == 0 || k == S.max_iterations) {
+      PROF_T0(t_chk);
       Residuals R = unscaled_residuals(team, P, F, ws, c, gnorm);
       team.sync();
+      PROF_ADD(ws, PF_CHECK, t_chk);
       if (R.pri <= S.eps_abs + S.eps_rel * R.ps && R.dua <= S.eps_abs + S.eps_rel * R.ds) break;
       if (k % S.check_interval == 0) {
         infeas = infeasible(team, P, F, ws, c);
@@ -689,6 +704,10 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
       }
     }
   }
+  PROF_ADD(ws, PF_ITER, t_iter);
+#if defined(__CUDA_ARCH__) && defined(ACCFEM_PROFILE)
+  if (ws.prof && team.rank() == 0) ws.prof[PF_ITERS] += (k > S.max_iterations ? S.max_iterations : k);
+#endif
   if (k > S.max_iterations) k = S.max_iterations;
   if (infeas) return ST_INFEASIBLE;
   Residuals R = unscaled_residuals(team, P, F, ws, c, gnorm);
@@ -700,7 +719,9 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   res.converged = (R.pri <= S.eps_abs + S.eps_rel * R.ps && R.dua <= S.eps_abs + S.eps_rel * R.ds) ? 1 : 0;
   res.rho_est = (S.adaptive_rho && k >= 3 * S.check_interval) ? rho_est : -1.0;
   if (S.polish && res.converged) {
+    PROF_T0(t_pol);
     int st = polish(team, P, F, ws, res, cmax);
+    PROF_ADD(ws, PF_POLISH, t_pol);
     if (st != ST_OK) return st;
   }
   return res.converged ? ST_OK : ST_NONCONV;

@@ -24,6 +24,18 @@
 
 #define PARFOR(i, n) for (int i = team.rank(); i < (n); i += team.size())
 
+// phase timers (development builds with -DACCFEM_PROFILE only)
+#if defined(__CUDA_ARCH__) && defined(ACCFEM_PROFILE)
+#define PROF_T0(v) long long v = clock64()
+#define PROF_ADD(ws, k, v) \
+  do { if ((ws).prof && team.rank() == 0) (ws).prof[k] += (unsigned long long)(clock64() - (v)); } while (0)
+#else
+#define PROF_T0(v)
+#define PROF_ADD(ws, k, v)
+#endif
+enum ProfPhase { PF_ELEMENT = 0, PF_DETECT, PF_RUIZ, PF_FACTOR, PF_ITER, PF_CHAIN, PF_CHECK, PF_POLISH, PF_DIRECT,
+                 PF_POST, PF_TOTAL, PF_ITERS, PF_FRAMES, PF_COUNT = 16 };
+
 namespace accfem {
 
 #if defined(__CUDACC__)

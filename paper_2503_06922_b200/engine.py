@@ -55,8 +55,11 @@ class BatchResult:
     trace_stats: object = None
 
     def to_numpy(self):
+        from dataclasses import fields
+
         out = {}
-        for k, v in self.__dict__.items():
+        for fd in fields(self):
+            k, v = fd.name, getattr(self, fd.name)
             if v is None:
                 out[k] = None
             elif hasattr(v, "detach"):
