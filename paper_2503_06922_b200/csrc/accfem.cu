@@ -31,10 +31,17 @@ __global__ void k_model_setup(int N, const double* rest, double* rest_dir, doubl
   model_setup(team, N, rest, rest_dir, rest_len, rest_frames, offsets, qa, qb, bad);
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride) {
+// persistent solve; one warp = one scenario at a time.  With hot_stride > 0
+// each warp's hot arrays (factor, iterate, row state) live in its slice of
+// dynamic shared memory; otherwise everything is in the global slab.
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride, long hot_stride) {
+  extern __shared__ double smem[];
   TeamWarp team{(int)(threadIdx.x & 31)};
-  const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, B.cmax_polish);
+  const int wib = threadIdx.x >> 5;
+  const long wid = (long)blockIdx.x * (blockDim.x >> 5) + wib;
+  double* hot = hot_stride > 0 ? smem + wib * hot_stride : nullptr;
+  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish);
   ws.prof = B.prof ? B.prof + wid * PF_COUNT : nullptr;
   while (true) {
     int s = 0;
@@ -50,7 +57,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
                    double* ws_base, long ws_stride, int* counter) {
   TeamWarp team{(int)(threadIdx.x & 31)};
   const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, 1);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, nullptr, P.m.N, P.m.n_fixed, 1);
   const int N = P.m.N, n = 6 * N, E = N - 1;
   while (true) {
     int s = 0;
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
              int* counter) {
   TeamWarp team{(int)(threadIdx.x & 31)};
   const long wid = (long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  Ws ws = ws_carve(ws_base + wid * ws_stride, P.m.N, 1);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, nullptr, P.m.N, P.m.n_fixed, 1);
   const int N = P.m.N, n = 6 * N;
   while (true) {
     int s = 0;
@@ -128,7 +135,9 @@ struct DevBuf {
 struct accfem_handle {
   int device = 0;
   int sms = 0;
-  int blocks_per_sm = 0;
+  int blocks_per_sm = 0;     // k_solve occupancy in the chosen mode
+  int solve_warps = 0;       // warps per k_solve block
+  long hot_stride = 0;       // doubles of shared memory per warp (0: global mode)
   int launches = 0;
   std::string err;
   Problem P;
@@ -295,8 +304,25 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
     delete h;
     return ACCFEM_E_DOMAIN;
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kWarpsPerBlock, 0);
-  if (h->blocks_per_sm < 1) h->blocks_per_sm = 1;
+  // launch mode: hot arrays in shared memory (one warp per block) when they fit
+  {
+    long hot = ws_hot_doubles(N, sd->n_fixed);
+    hot = (hot + 15) & ~15L;
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const char* force_global = getenv("ACCFEM_GLOBAL_WORKSPACE");
+    if (hot * 8 <= max_smem && !(force_global && force_global[0] == '1')) {
+      h->hot_stride = hot;
+      h->solve_warps = 1;
+      cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(hot * 8));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32, hot * 8);
+    } else {
+      h->hot_stride = 0;
+      h->solve_warps = kWarpsPerBlock;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kWarpsPerBlock, 0);
+    }
+    if (h->blocks_per_sm < 1) h->blocks_per_sm = 1;
+  }
   *out = h;
   return 0;
 }
@@ -318,7 +344,7 @@ extern "C" int accfem_destroy(accfem_handle* h) {
 
 // size the workspace for `teams` resident warps
 static int ensure_ws(accfem_handle* h, long teams, int cmax) {
-  long stride = ws_doubles(h->N, cmax);
+  long stride = ws_doubles(h->N, h->n_fixed, cmax);
   stride = (stride + 31) & ~31L;
   size_t need = (size_t)stride * teams;
   if (h->ws_stride != stride || h->ws.n < need) {
@@ -335,7 +361,7 @@ static long grid_blocks(accfem_handle* h, long S) {
   return std::max(1L, std::min(want, cap));
 }
 
-extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm * kWarpsPerBlock : 0; }
+extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm * h->solve_warps : 0; }
 extern "C" long long accfem_workspace_bytes(accfem_handle* h) { return h ? (long long)h->ws.n * 8 : 0; }
 extern "C" int accfem_launches(accfem_handle* h) { return h ? h->launches : 0; }
 
@@ -352,8 +378,9 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   }
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  long blocks = grid_blocks(h, io->S);
-  if (int rc = ensure_ws(h, blocks * kWarpsPerBlock, h->cmax)) return rc;
+  const long wpb = h->solve_warps;
+  long blocks = std::max(1L, std::min((io->S + wpb - 1) / wpb, (long)h->sms * h->blocks_per_sm));
+  if (int rc = ensure_ws(h, blocks * wpb, h->cmax)) return rc;
   BatchDev B;
   memset(&B, 0, sizeof(B));
   B.S = io->S;
@@ -374,7 +401,8 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
   B.prof = h->prof;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
-  k_solve<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, B, h->ws.p, h->ws_stride);
+  k_solve<<<(unsigned)blocks, 32 * (unsigned)wpb, (size_t)(h->hot_stride * 8 * wpb), st>>>(h->P, B, h->ws.p,
+                                                                                           h->ws_stride, h->hot_stride);
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
   return 0;

@@ -76,41 +76,52 @@ struct Ws {
   // contacts (indexed by node during detection, by contact after compaction)
   double *cgap, *cpp, *cnrm;
   int *ctri, *cnode, *crow_of_node;
-  // rows (fixed rows first, then contacts)
+  // rows (fixed rows first, then contacts); unscaled bounds lo/up, scaled ls/us
   double *lo, *up, *ls, *us, *e, *rho, *as, *z, *y, *yprev, *tr, *yfull, *warm;
-  // scaled system
+  // scaled system; HD/HU hold H_s, then M, then its twisted factor in place
   double *HD, *HU, *gs, *d, *colh, *xs, *xt, *rhs, *w, *v, *tmp;
-  // factors: ADMM (scaled) and direct / polish (unscaled)
-  double *Li, *G, *Hb, *Li2, *G2, *Hb2;
-  // solution
+  // solution / polish
   double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr;
   int *act, *alist;
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
 };
 
-constexpr int kMultiRhs = 5;  // right-hand sides solved concurrently by one warp (6 lanes each)
+constexpr int kMultiRhs = 2;  // right-hand sides solved concurrently by one warp (12 lanes each)
 
-HDEV Ws ws_carve(double* base, int N, int cmax_polish, long* used = nullptr) {
-  long n = 6L * N, E = N - 1, m = 7L * N;  // rows: <= 6N selector rows + N node contacts
+// Carve a team's workspace.  Arrays touched by every ADMM iteration (the
+// factor, the scaled iterate and the row state) come from `hot` (shared
+// memory on the device) when given, else from the global slab `base`.
+// Either base may be null to measure: *used / *hot_used receive the sizes.
+HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long* used = nullptr,
+                 long* hot_used = nullptr) {
+  long n = 6L * N, E = N - 1, m = (long)nf + N;  // rows: selector rows + at most one contact per node
   long cp = cmax_polish;
   Ws w;
-  double* p = base;
-  long off = 0;
-  auto take = [&](long k) { double* r = p ? p + off : nullptr; off += (k + 3) & ~3L; return r; };
+  long off = 0, hoff = 0;
+  auto take = [&](long k) { double* r = base ? base + off : nullptr; off += (k + 3) & ~3L; return r; };
+  auto takeh = [&](long k) {
+    if (!hot) return take(k);
+    double* r = hot + hoff;
+    hoff += (k + 1) & ~1L;
+    return r;
+  };
+  // hot
+  w.HD = takeh(36L * N); w.HU = takeh(36 * E);
+  w.xs = takeh(n); w.gs = takeh(n); w.rhs = takeh(n); w.tmp = takeh(n);
+  w.xt = w.rhs;  // the solve writes its result over the right-hand side
+  w.z = takeh(m); w.y = takeh(m); w.yprev = takeh(m); w.rho = takeh(m); w.ls = takeh(m); w.us = takeh(m);
+  w.tr = takeh(m); w.as = takeh(3 * m);
+  // cold
   w.R = take(9L * N); w.frames = take(9 * E); w.fe = take(12 * E); w.ke = take(108 * E);
   w.fint = take(n); w.KD = take(36L * N); w.KU = take(36 * E);
   w.fa = take(n); w.g = take(n); w.rres = take(n);
   w.cgap = take(N); w.cpp = take(3L * N); w.cnrm = take(3L * N);
-  w.lo = take(m); w.up = take(m); w.ls = take(m); w.us = take(m); w.e = take(m); w.rho = take(m); w.as = take(3 * m);
-  w.z = take(m); w.y = take(m); w.yprev = take(m); w.tr = take(m); w.yfull = take(m); w.warm = take(N);
-  w.HD = take(36L * N); w.HU = take(36 * E); w.gs = take(n); w.d = take(n); w.colh = take(n);
-  w.xs = take(n); w.xt = take(n); w.rhs = take(n); w.w = take(n); w.v = take(n); w.tmp = take(n);
-  w.Li = take(36L * N); w.G = take(36L * N); w.Hb = take(36L * N);
-  w.Li2 = take(36L * N); w.G2 = take(36L * N); w.Hb2 = take(36L * N);
-  w.dx = take(n); w.dxp = take(n); w.yp = take(m); w.S = take(cp * cp); w.Sy = take(cp);
-  w.Wc = take(kMultiRhs * n);
+  w.lo = take(m); w.up = take(m); w.e = take(m); w.yfull = take(m); w.warm = take(N);
+  w.d = take(n); w.colh = take(n); w.w = take(n); w.v = take(n);
+  w.dx = take(n); w.dxp = take(n); w.yp = take(m); w.S = take(cp * cp); w.Sy = take(3 * cp);
+  w.Wc = take(2 * kMultiRhs * n);
   w.wfix = take(n);
-  w.scr = take(128);
+  w.scr = take(160);
   double* ib = take((5L * N + m + 8) / 2 + 1);
   int* ip = reinterpret_cast<int*>(ib);
   w.ctri = ip; ip = ip ? ip + N : nullptr;
@@ -120,13 +131,21 @@ HDEV Ws ws_carve(double* base, int N, int cmax_polish, long* used = nullptr) {
   w.alist = ip;
   w.prof = nullptr;
   if (used) *used = off;
+  if (hot_used) *hot_used = hot ? hoff : 0;
   return w;
 }
 
-HDEV long ws_doubles(int N, int cmax_polish) {
+HDEV long ws_doubles(int N, int nf, int cmax_polish) {
   long used = 0;
-  ws_carve(nullptr, N, cmax_polish, &used);
+  ws_carve(nullptr, nullptr, N, nf, cmax_polish, &used);
   return used;
+}
+
+// hot-region size (doubles) of one team
+HDEV long ws_hot_doubles(int N, int nf) {
+  long n = 6L * N, m = (long)nf + N;
+  auto r2 = [](long k) { return (k + 1) & ~1L; };
+  return r2(36L * N) + r2(36L * (N - 1)) + 4 * r2(n) + 7 * r2(m) + r2(3 * m);
 }
 
 // ---------------------------------------------------------------------------

@@ -254,7 +254,8 @@ DEV bool infeasible(const Team& team, const Problem& P, const Frame& F, Ws& ws, 
 
 // ---------------------------------------------------------------------------
 // reduced unscaled factor for the direct / polish solves: H (+ delta I on free
-// DOFs) with selector DOFs replaced by identity rows/columns -> Li2/G2/Hb2
+// DOFs) with selector DOFs replaced by identity rows/columns, factored in place
+// in HD/HU
 // ---------------------------------------------------------------------------
 template <class Team>
 DEV int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws) {
@@ -274,7 +275,7 @@ DEV int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws)
     ws.HU[i] = (fr || fc) ? 0.0 : ws.KU[i];
   }
   team.sync();
-  return block_factor(team, N, ws.HD, ws.HU, ws.Li2, ws.G2, ws.Hb2, ws.scr);
+  return twisted_factor(team, N, ws.HD, ws.HU, ws.scr);
 }
 
 // full-length rhs for the eliminated system: b at selector DOFs,
@@ -321,7 +322,7 @@ DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws,
   const int N = P.m.N, n = 6 * N;
   if (reduced_factor(team, P, 0.0, ws) >= 0) return ST_LINALG;
   eliminated_rhs(team, P, F, ws, ws.rhs);
-  chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.rhs, ws.dx, 1, 0);
+  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.dx, 1, 0);
   team.sync();
   for (int it = 0; it < 3; ++it) {
     block_matvec(team, N, ws.KD, ws.KU, ws.dx, ws.tmp);
@@ -330,7 +331,7 @@ DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws,
       ws.rhs[j] = fx ? 0.0 : -ws.g[j] - ws.tmp[j];
     }
     team.sync();
-    chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.rhs, ws.w, 1, 0);
+    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0);
     team.sync();
     PARFOR(j, n) ws.dx[j] += ws.w[j];
     team.sync();
@@ -399,7 +400,7 @@ template <class Team>
 DEV void schur_solve(const Team& team, const Problem& P, Ws& ws, int na, const double* f, const double* h,
                      double* xo, double* yo) {
   const int N = P.m.N, n = 6 * N;
-  chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, f, ws.v, 1, 0);
+  twisted_solve(team, N, ws.HD, ws.HU, f, ws.tmp, ws.v, 1, 0);
   team.sync();
   PARFOR(q, na) {
     int c = ws.alist[q];
@@ -421,7 +422,7 @@ DEV void schur_solve(const Team& team, const Problem& P, Ws& ws, int na, const d
     }
   }
   team.sync();
-  chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.rhs, ws.w, 1, 0);
+  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0);
   team.sync();
   PARFOR(j, n) xo[j] = ws.v[j] - ws.w[j];
   team.sync();
@@ -479,7 +480,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
         }
       }
       team.sync();
-      chain_solve(team, N, ws.Li2, ws.G2, ws.Hb2, ws.Wc, ws.Wc, nb, n);
+      twisted_solve(team, N, ws.HD, ws.HU, ws.Wc, ws.Wc + kMultiRhs * n, ws.Wc, nb, n);
       team.sync();
       PARFOR(t, na * nb) {
         int p = t / nb, b = t % nb;
@@ -503,7 +504,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     eliminated_rhs(team, P, F, ws, ws.xt);
     PARFOR(q, na) ws.Sy[q] = ws.up[nf + ws.alist[q]];
     team.sync();
-    double* yact = ws.tr;  // na entries
+    double* yact = ws.Sy + cmax;  // na entries
     schur_solve(team, P, ws, na, ws.xt, ws.Sy, dxp, yact);
     // one refinement round against the exact KKT
     PARFOR(j, n) ws.tmp[j] = 0.0;
@@ -524,7 +525,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
       ws.Sy[q] = ws.up[nf + c] - row_dot(P, F, ws, nf + c, dxp);
     }
     team.sync();
-    double* dyq = ws.tr + na;
+    double* dyq = ws.Sy + 2 * cmax;
     schur_solve(team, P, ws, na, ws.xt, ws.Sy, ws.colh, dyq);
     PARFOR(j, n) dxp[j] += ws.colh[j];
     PARFOR(q, na) yact[q] += dyq[q];
@@ -633,7 +634,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   }
   team.sync();
   PROF_T0(t_fac);
-  int fbad = block_factor(team, N, ws.HD, ws.HU, ws.Li, ws.G, ws.Hb, ws.scr);
+  int fbad = twisted_factor(team, N, ws.HD, ws.HU, ws.scr);
   PROF_ADD(ws, PF_FACTOR, t_fac);
   if (fbad >= 0) return ST_LINALG;
   // initial iterate (solver.py:287-289)
@@ -667,7 +668,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     }
     team.sync();
     PROF_T0(t_ch);
-    chain_solve(team, N, ws.Li, ws.G, ws.Hb, ws.rhs, ws.xt, 1, 0);
+    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0);
     team.sync();
     PROF_ADD(ws, PF_CHAIN, t_ch);
     PARFOR(r, m) {

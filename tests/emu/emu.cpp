@@ -85,7 +85,7 @@ extern "C" EmuHandle* emu_create(const accfem_model_desc* md, const accfem_mesh_
     for (int a = 0; a < 3; ++a) { G.origin[a] = h->mesh.origin[a]; G.dims[a] = h->mesh.dims[a]; }
     G.inv_h = h->mesh.inv_h;
   }
-  h->ws.assign(ws_doubles(N, h->cmax) + 64, 0.0);
+  h->ws.assign(ws_doubles(N, sd->n_fixed, h->cmax) + 64, 0.0);
   return h;
 }
 
@@ -93,7 +93,7 @@ extern "C" void emu_destroy(EmuHandle* h) { delete h; }
 
 extern "C" int emu_element_pass(EmuHandle* h, int S, const double* x, double* fint, double* kd, double* ku, int* bad) {
   const int N = h->N, n = 6 * N, E = N - 1;
-  Ws ws = ws_carve(h->ws.data(), N, h->cmax);
+  Ws ws = ws_carve(h->ws.data(), nullptr, N, h->n_fixed, h->cmax);
   for (int s = 0; s < S; ++s) {
     int b = element_pass(TeamSerial{}, h->P, x + (long)s * n, ws, true);
     bad[s] = b;
@@ -107,7 +107,7 @@ extern "C" int emu_element_pass(EmuHandle* h, int S, const double* x, double* fi
 
 extern "C" int emu_detect(EmuHandle* h, int S, const double* x, int* tri, double* gap, double* point) {
   const int N = h->N, n = 6 * N;
-  Ws ws = ws_carve(h->ws.data(), N, h->cmax);
+  Ws ws = ws_carve(h->ws.data(), nullptr, N, h->n_fixed, h->cmax);
   for (int s = 0; s < S; ++s) {
     int nc = detect_pass(TeamSerial{}, h->P, x + (long)s * n, ws);
     for (int k = 0; k < N; ++k) tri[(long)s * N + k] = -1;
@@ -138,7 +138,7 @@ extern "C" int emu_solve_batch(EmuHandle* h, const accfem_batch* io) {
   B.trace_c_point = io->trace_contact_point;
   B.max_frames = io->max_frames; B.stop_on_tol = io->stop_on_tol; B.tol = io->tol;
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax;
-  Ws ws = ws_carve(h->ws.data(), h->N, h->cmax);
+  Ws ws = ws_carve(h->ws.data(), nullptr, h->N, h->n_fixed, h->cmax);
   for (int s = 0; s < io->S; ++s) run_scenario(TeamSerial{}, h->P, B, s, ws);
   return 0;
 }
