@@ -16,40 +16,52 @@
 
 namespace accfem {
 
-// symmetric positive definite 6x6 inverse (Cholesky); false on a non-positive pivot
+// symmetric positive definite 6x6 inverse via LDL^T (six reciprocals, no
+// square roots; fully unrolled so everything stays in registers).  Writes
+// the full symmetric inverse; false on a non-positive pivot.
 DEV bool spd6_inv(const double* S, double* Inv) {
-  double L[21];  // packed lower, row-major: (r, c) at r*(r+1)/2 + c
+  double L[15];  // strictly lower, packed: (i, j), j < i, at i*(i-1)/2 + j
+  double d[6], di[6];
+  bool ok = true;
+#pragma unroll
   for (int j = 0; j < 6; ++j) {
-    double dj = S[6 * j + j];
-    for (int k = 0; k < j; ++k) dj -= L[j * (j + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
-    if (!(dj > 0.0)) return false;
-    double ljj = sqrt(dj);
-    L[j * (j + 1) / 2 + j] = ljj;
-    double inv = 1.0 / ljj;
+    double a = S[6 * j + j];
+#pragma unroll
+    for (int q = 0; q < j; ++q) a -= L[j * (j - 1) / 2 + q] * (L[j * (j - 1) / 2 + q] * d[q]);
+    ok = ok && (a > 0.0);
+    d[j] = a;
+    di[j] = 1.0 / a;
+#pragma unroll
     for (int i = j + 1; i < 6; ++i) {
-      double s = S[6 * i + j];
-      for (int k = 0; k < j; ++k) s -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
-      L[i * (i + 1) / 2 + j] = s * inv;
+      double t = S[6 * i + j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) t -= L[i * (i - 1) / 2 + q] * (L[j * (j - 1) / 2 + q] * d[q]);
+      L[i * (i - 1) / 2 + j] = t * di[j];
     }
   }
-  // W = L^{-1} (lower), Inv = W^T W
-  double W[21];
-  for (int c = 0; c < 6; ++c) {
-    W[c * (c + 1) / 2 + c] = 1.0 / L[c * (c + 1) / 2 + c];
-    for (int r = c + 1; r < 6; ++r) {
-      double s = 0.0;
-      for (int k = c; k < r; ++k) s += L[r * (r + 1) / 2 + k] * W[k * (k + 1) / 2 + c];
-      W[r * (r + 1) / 2 + c] = -s / L[r * (r + 1) / 2 + r];
+  // W = L^{-1} (unit lower): W_ij = -sum_{q=j}^{i-1} L_iq W_qj
+  double W[15];
+#pragma unroll
+  for (int i = 1; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      double t = -L[i * (i - 1) / 2 + j];
+#pragma unroll
+      for (int q = j + 1; q < i; ++q) t -= L[i * (i - 1) / 2 + q] * W[q * (q - 1) / 2 + j];
+      W[i * (i - 1) / 2 + j] = t;
     }
-  }
+  // Inv = W^T D^{-1} W: Inv_rc = sum_{q >= max(r, c)} W_qr W_qc / d_q
+#pragma unroll
   for (int r = 0; r < 6; ++r)
+#pragma unroll
     for (int c = r; c < 6; ++c) {
-      double s = 0.0;
-      for (int k = c; k < 6; ++k) s += W[k * (k + 1) / 2 + r] * W[k * (k + 1) / 2 + c];
-      Inv[6 * r + c] = s;
-      Inv[6 * c + r] = s;
+      double t = (c == r) ? di[r] : W[c * (c - 1) / 2 + r] * di[c];
+#pragma unroll
+      for (int q = c + 1; q < 6; ++q) t += W[q * (q - 1) / 2 + r] * (W[q * (q - 1) / 2 + c] * di[q]);
+      Inv[6 * r + c] = t;
+      Inv[6 * c + r] = t;
     }
-  return true;
+  return ok;
 }
 
 DEV int twist_split(int N) { return (N - 1) / 2; }
@@ -149,7 +161,8 @@ DEV int twisted_factor(const TeamSerial&, int N, double* D, double* U, double* s
 }
 
 // Solve M x = r for `nrhs` right-hand sides: r_g = rhs + g*stride, result to
-// out + g*stride (out may alias rhs); tmp (same layout) holds the sweep-1 values.
+// out + g*stride; tmp (same layout) holds the sweep-1 values.  out may alias
+// rhs or tmp.
 DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* U, const double* rhs, double* tmp,
                        double* out, int nrhs, long stride) {
   const int k = twist_split(N);
@@ -157,25 +170,22 @@ DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* 
     const double* b = rhs + g * stride;
     double* v = tmp + g * stride;
     double* x = out + g * stride;
-    for (int r = 0; r < 6; ++r) v[r] = b[r];
-    for (int i = 1; i < k; ++i) {
-      const double* X = U + 36 * (i - 1);
+    // sweep 1, top: v_i = b_i - X_i v_{i-1};  bottom: u_i = b_i - Y_i u_{i+1}
+    for (int i = 0; i < k; ++i)
       for (int r = 0; r < 6; ++r) {
         double a = b[6 * i + r];
-        for (int j = 0; j < 6; ++j) a -= X[6 * r + j] * v[6 * (i - 1) + j];
+        if (i > 0)
+          for (int j = 0; j < 6; ++j) a -= U[36 * (i - 1) + 6 * r + j] * v[6 * (i - 1) + j];
         v[6 * i + r] = a;
       }
-    }
-    for (int r = 0; r < 6; ++r) v[6 * (N - 1) + r] = b[6 * (N - 1) + r];
-    for (int i = N - 2; i > k; --i) {
-      const double* Y = U + 36 * i;
+    for (int i = N - 1; i > k; --i)
       for (int r = 0; r < 6; ++r) {
         double a = b[6 * i + r];
-        for (int j = 0; j < 6; ++j) a -= Y[6 * r + j] * v[6 * (i + 1) + j];
+        if (i < N - 1)
+          for (int j = 0; j < 6; ++j) a -= U[36 * i + 6 * r + j] * v[6 * (i + 1) + j];
         v[6 * i + r] = a;
       }
-    }
-    double t[6];
+    double t[6], xk[6];
     for (int r = 0; r < 6; ++r) {
       double pt = 0.0, pb = 0.0;
       if (k > 0)
@@ -184,229 +194,273 @@ DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* 
         for (int j = 0; j < 6; ++j) pb += U[36 * k + 6 * r + j] * v[6 * (k + 1) + j];
       t[r] = b[6 * k + r] - (pt + pb);
     }
-    double xk[6];
     for (int r = 0; r < 6; ++r) {
       double a = 0.0;
       for (int j = 0; j < 6; ++j) a += D[36 * k + 6 * r + j] * t[j];
       xk[r] = a;
     }
+    // z_i = Dinv_i v_i (in place)
+    for (int i = 0; i < N; ++i) {
+      if (i == k) continue;
+      double z[6];
+      for (int r = 0; r < 6; ++r) {
+        double a = 0.0;
+        for (int j = 0; j < 6; ++j) a += D[36 * i + 6 * r + j] * v[6 * i + j];
+        z[r] = a;
+      }
+      for (int r = 0; r < 6; ++r) v[6 * i + r] = z[r];
+    }
     for (int r = 0; r < 6; ++r) x[6 * k + r] = xk[r];
-    for (int i = k - 1; i >= 0; --i) {
-      const double* X = U + 36 * i;  // X_{i+1}
+    // sweep 2, top: x_i = z_i - X_{i+1}^T x_{i+1};  bottom: x_i = z_i - Y_{i-1}^T x_{i-1}
+    for (int i = k - 1; i >= 0; --i)
       for (int r = 0; r < 6; ++r) {
-        double a = 0.0;
-        for (int j = 0; j < 6; ++j) a += D[36 * i + 6 * r + j] * v[6 * i + j];
-        for (int j = 0; j < 6; ++j) a -= X[6 * j + r] * x[6 * (i + 1) + j];
+        double a = v[6 * i + r];
+        for (int j = 0; j < 6; ++j) a -= U[36 * i + 6 * j + r] * x[6 * (i + 1) + j];
         x[6 * i + r] = a;
       }
-    }
-    for (int i = k + 1; i < N; ++i) {
-      const double* Y = U + 36 * (i - 1);  // Y_{i-1}
+    for (int i = k + 1; i < N; ++i)
       for (int r = 0; r < 6; ++r) {
-        double a = 0.0;
-        for (int j = 0; j < 6; ++j) a += D[36 * i + 6 * r + j] * v[6 * i + j];
-        for (int j = 0; j < 6; ++j) a -= Y[6 * j + r] * x[6 * (i - 1) + j];
+        double a = v[6 * i + r];
+        for (int j = 0; j < 6; ++j) a -= U[36 * (i - 1) + 6 * j + r] * x[6 * (i - 1) + j];
         x[6 * i + r] = a;
       }
-    }
   }
 }
 
 #if defined(__CUDACC__)
-// Warp factorisation: lanes 0-15 run the top recursion, lanes 16-31 the
-// bottom one; within a half, lane l owns entries l and l+16 of each 6x6
-// product, and every lane of the half inverts the Schur block redundantly.
+// 6x6 helpers on register arrays
+DEV void ld36(const double* __restrict__ p, double* a) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 18; ++i) {
+    double2 v = q[i];
+    a[2 * i] = v.x;
+    a[2 * i + 1] = v.y;
+  }
+}
+DEV void st36(double* p, const double* a) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 18; ++i) q[i] = make_double2(a[2 * i], a[2 * i + 1]);
+}
+DEV void ld6(const double* __restrict__ p, double* a) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double2 v = q[i];
+    a[2 * i] = v.x;
+    a[2 * i + 1] = v.y;
+  }
+}
+DEV void st6(double* p, const double* a) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) q[i] = make_double2(a[2 * i], a[2 * i + 1]);
+}
+
+// one Schur step on a single lane: X = C^T P (top) or C P (bottom), S = A - X C
+// (top) or A - X C^T (bottom); X written to Xout, inverse of S to Dout
+DEV bool schur_step(bool top, const double* A, const double* C, const double* P, double* Xout, double* Dout) {
+  double X[36], S[36];
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a += (top ? C[6 * q + r] : C[6 * r + q]) * P[6 * q + c];
+      X[6 * r + c] = a;
+    }
+  st36(Xout, X);
+  ld36(A, S);
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double a = S[6 * r + c];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * (top ? C[6 * q + c] : C[6 * c + q]);
+      S[6 * r + c] = a;
+    }
+  double Inv[36];
+  bool ok = spd6_inv(S, Inv);
+  st36(Dout, Inv);
+  return ok;
+}
+
+// Warp factorisation: lane 0 runs the top recursion, lane 1 the bottom one,
+// each 6x6 step entirely in registers; they meet at the middle block.
 DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double* scratch) {
   const int lane = team.lane;
-  const int half = lane >> 4, hl = lane & 15;
   const int k = twist_split(N);
-  double* Xs = scratch + 72 * half;  // per-half product scratch
-  double* Ss = Xs + 36;
-  const int steps = k > (N - 1 - k) ? k : (N - 1 - k);
-  int fail = -1;
-  for (int t = 0; t < steps; ++t) {
-    // top step i = t (< k); bottom step i = N-1-t (> k)
-    int i = half == 0 ? t : N - 1 - t;
-    bool act = half == 0 ? (t < k) : (N - 1 - t > k);
-    bool first = (t == 0);
-    const double* C = half == 0 ? U + 36 * (i - 1) : U + 36 * i;
-    const double* Pn = half == 0 ? D + 36 * (i - 1) : D + 36 * (i + 1);  // previous inverse
-    if (act && !first) {
-      for (int e = hl; e < 36; e += 16) {
-        int r = e / 6, c = e % 6;
-        double a = 0.0;
-        if (half == 0)
-          for (int q = 0; q < 6; ++q) a += C[6 * q + r] * Pn[6 * q + c];
-        else
-          for (int q = 0; q < 6; ++q) a += C[6 * r + q] * Pn[6 * q + c];
-        Xs[e] = a;
+  int fail = 1 << 30;
+  if (lane < 2) {
+    const bool top = lane == 0;
+    const int cnt = top ? k : N - 1 - k;
+    for (int t = 0; t < cnt; ++t) {
+      const int i = top ? t : N - 1 - t;
+      bool ok;
+      if (t == 0) {
+        double S[36], Inv[36];
+        ld36(D + 36 * i, S);
+        ok = spd6_inv(S, Inv);
+        st36(D + 36 * i, Inv);
+      } else {
+        double C[36], P[36];
+        double* Cp = top ? U + 36 * (i - 1) : U + 36 * i;
+        ld36(Cp, C);
+        ld36(top ? D + 36 * (i - 1) : D + 36 * (i + 1), P);
+        ok = schur_step(top, D + 36 * i, C, P, Cp, D + 36 * i);
       }
+      if (!ok && fail == (1 << 30)) fail = i;
     }
-    __syncwarp();
-    if (act) {
-      for (int e = hl; e < 36; e += 16) {
-        int r = e / 6, c = e % 6;
-        double a = D[36 * i + e];
-        if (!first) {
-          if (half == 0)
-            for (int q = 0; q < 6; ++q) a -= Xs[6 * r + q] * C[6 * q + c];
-          else
-            for (int q = 0; q < 6; ++q) a -= Xs[6 * r + q] * C[6 * c + q];
+    // middle contributions X_k C_{k-1} (top) and Y_k C_k^T (bottom)
+    double part[36];
+#pragma unroll
+    for (int e = 0; e < 36; ++e) part[e] = 0.0;
+    if (cnt > 0) {
+      double C[36], P[36], X[36];
+      double* Cp = top ? U + 36 * (k - 1) : U + 36 * k;
+      ld36(Cp, C);
+      ld36(top ? D + 36 * (k - 1) : D + 36 * (k + 1), P);
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < 6; ++q) a += (top ? C[6 * q + r] : C[6 * r + q]) * P[6 * q + c];
+          X[6 * r + c] = a;
         }
-        Ss[e] = a;
-      }
-    }
-    __syncwarp();
-    if (act) {
-      double Sr[36], Inv[36];
-      for (int e = 0; e < 36; ++e) Sr[e] = Ss[e];
-      bool ok = spd6_inv(Sr, Inv);
-      if (!ok && fail < 0) fail = i;
-      for (int e = hl; e < 36; e += 16) {
-        D[36 * i + e] = Inv[e];
-        if (!first) {
-          if (half == 0) U[36 * (i - 1) + e] = Xs[e];
-          else U[36 * i + e] = Xs[e];
+      st36(Cp, X);
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < 6; ++q) a += X[6 * r + q] * (top ? C[6 * q + c] : C[6 * c + q]);
+          part[6 * r + c] = a;
         }
-      }
     }
-    __syncwarp();
+    st36(scratch + 36 * lane, part);
   }
-  // middle block: lanes 0-15 form X_k C_{k-1}, lanes 16-31 Y_k C_k^T
-  {
-    const bool has = half == 0 ? (k > 0) : (k < N - 1);
-    const double* C = half == 0 ? U + 36 * (k - 1) : U + 36 * k;
-    const double* Pn = half == 0 ? D + 36 * (k - 1) : D + 36 * (k + 1);
-    if (has) {
-      for (int e = hl; e < 36; e += 16) {
-        int r = e / 6, c = e % 6;
-        double a = 0.0;
-        if (half == 0)
-          for (int q = 0; q < 6; ++q) a += C[6 * q + r] * Pn[6 * q + c];
-        else
-          for (int q = 0; q < 6; ++q) a += C[6 * r + q] * Pn[6 * q + c];
-        Xs[e] = a;
-      }
-    }
-    __syncwarp();
-    if (has) {
-      for (int e = hl; e < 36; e += 16) {
-        int r = e / 6, c = e % 6;
-        double a = 0.0;
-        if (half == 0)
-          for (int q = 0; q < 6; ++q) a += Xs[6 * r + q] * C[6 * q + c];
-        else
-          for (int q = 0; q < 6; ++q) a += Xs[6 * r + q] * C[6 * c + q];
-        Ss[e] = a;
-      }
-    } else {
-      for (int e = hl; e < 36; e += 16) Ss[e] = 0.0;
-    }
-    __syncwarp();
-    double Sr[36], Inv[36];
-    for (int e = 0; e < 36; ++e) Sr[e] = D[36 * k + e] - scratch[36 + e] - scratch[72 + 36 + e];
-    bool ok = spd6_inv(Sr, Inv);
-    if (!ok && fail < 0) fail = k;
-    __syncwarp();
-    if (lane < 16) {
-      for (int e = hl; e < 36; e += 16) {
-        D[36 * k + e] = Inv[e];
-        if (k > 0) U[36 * (k - 1) + e] = scratch[e];
-      }
-    } else {
-      for (int e = hl; e < 36; e += 16)
-        if (k < N - 1) U[36 * k + e] = scratch[72 + e];
-    }
-    __syncwarp();
+  __syncwarp();
+  if (lane == 0) {
+    double S[36], Pt[36], Pb[36], Inv[36];
+    ld36(D + 36 * k, S);
+    ld36(scratch, Pt);
+    ld36(scratch + 36, Pb);
+#pragma unroll
+    for (int e = 0; e < 36; ++e) S[e] = S[e] - (Pt[e] + Pb[e]);
+    bool ok = spd6_inv(S, Inv);
+    st36(D + 36 * k, Inv);
+    if (!ok && fail == (1 << 30)) fail = k;
   }
-  int worst = team.imin(fail < 0 ? (1 << 30) : fail);
+  __syncwarp();
+  int worst = team.imin(fail);
   return worst == (1 << 30) ? -1 : worst;
 }
 
-// Warp solve: a group of 12 lanes per right-hand side (g < 2): lanes 0-5 sweep
-// the top half, lanes 6-11 the bottom half; lane row r = lane % 6.  Both
-// halves run the same trip count (the shorter one idles on its last step) so
-// every shuffle is warp-uniform.  out must not alias tmp.
+// Warp solve: right-hand side g (< 16) is swept by lanes 2g (top half) and
+// 2g+1 (bottom half); each step is a full 6x6 mat-vec in one lane's
+// registers, so the recurrence carries no shuffles.  The independent
+// z_i = Dinv_i v_i products run across all lanes between the sweeps.
 DEV void twisted_solve(const TeamWarp& team, int N, const double* __restrict__ D, const double* __restrict__ U,
                        const double* rhs, double* tmp, double* out, int nrhs, long stride) {
   const int lane = team.lane;
-  const int g = lane / 12, sub = (lane % 12) / 6, r = lane % 6;
-  const bool act = g < nrhs && lane < 24;
-  const int gg = act ? g : 0;
-  const double* b = rhs + gg * stride;
-  double* v = tmp + gg * stride;
-  double* x = out + gg * stride;
+  const int g = lane >> 1;
+  const bool top = (lane & 1) == 0;
+  const bool act = g < nrhs;
   const int k = twist_split(N);
-  const int grp = 12 * (g < 2 ? g : 0);
-  const int base = grp + 6 * sub;       // my half
-  const int other = grp + 6 * (1 - sub);
-  const int my_n = sub == 0 ? k : N - 1 - k;
-  const int steps = (N - 1 - k) > k ? (N - 1 - k) : k;
-  // sweep 1: top i = 0..k-1 (v_i = b_i - X_i v_{i-1}); bottom i = N-1..k+1 (u_i = b_i - Y_i u_{i+1})
-  double prev = 0.0;
-  for (int t = 0; t < steps; ++t) {
-    const bool live = t < my_n;
-    const int i = sub == 0 ? t : N - 1 - t;
-    double a = live ? b[6 * i + r] : 0.0;
-    if (t > 0) {
-      double p0 = __shfl_sync(0xffffffffu, prev, base + 0), p1 = __shfl_sync(0xffffffffu, prev, base + 1);
-      double p2 = __shfl_sync(0xffffffffu, prev, base + 2), p3 = __shfl_sync(0xffffffffu, prev, base + 3);
-      double p4 = __shfl_sync(0xffffffffu, prev, base + 4), p5 = __shfl_sync(0xffffffffu, prev, base + 5);
-      if (live) {
-        const double* M = sub == 0 ? U + 36 * (i - 1) + 6 * r : U + 36 * i + 6 * r;
-        double a1 = M[1] * p1 + M[3] * p3 + M[5] * p5;
-        a -= M[0] * p0 + M[2] * p2 + M[4] * p4 + a1;
+  const int cnt = top ? k : N - 1 - k;
+  const double* b = rhs + (act ? g : 0) * stride;
+  double* v = tmp + (act ? g : 0) * stride;
+  double* x = out + (act ? g : 0) * stride;
+  double p[6] = {0, 0, 0, 0, 0, 0};
+  if (act) {
+    for (int t = 0; t < cnt; ++t) {
+      const int i = top ? t : N - 1 - t;
+      double a[6];
+      ld6(b + 6 * i, a);
+      if (t > 0) {
+        double M[36];
+        ld36(top ? U + 36 * (i - 1) : U + 36 * i, M);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          double s0 = M[6 * r] * p[0] + M[6 * r + 2] * p[2] + M[6 * r + 4] * p[4];
+          double s1 = M[6 * r + 1] * p[1] + M[6 * r + 3] * p[3] + M[6 * r + 5] * p[5];
+          a[r] -= s0 + s1;
+        }
       }
-    }
-    if (live) {
-      prev = a;
-      if (act) v[6 * i + r] = a;
+#pragma unroll
+      for (int r = 0; r < 6; ++r) p[r] = a[r];
+      st6(v + 6 * i, a);
     }
   }
-  // middle: x_k = Z^{-1} (b_k - (X_k v_{k-1} + Y_k u_{k+1}))
-  double part = 0.0;
+  // middle block: x_k = Zinv (b_k - (X_k v_{k-1} + Y_k u_{k+1}))
+  double part[6] = {0, 0, 0, 0, 0, 0};
+  if (act && cnt > 0) {
+    double M[36];
+    ld36(top ? U + 36 * (k - 1) : U + 36 * k, M);
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+      part[r] = M[6 * r] * p[0] + M[6 * r + 1] * p[1] + M[6 * r + 2] * p[2] + M[6 * r + 3] * p[3] +
+                M[6 * r + 4] * p[4] + M[6 * r + 5] * p[5];
+  }
+  double xk[6];
   {
-    const bool has = my_n > 0;
-    double p0 = __shfl_sync(0xffffffffu, prev, base + 0), p1 = __shfl_sync(0xffffffffu, prev, base + 1);
-    double p2 = __shfl_sync(0xffffffffu, prev, base + 2), p3 = __shfl_sync(0xffffffffu, prev, base + 3);
-    double p4 = __shfl_sync(0xffffffffu, prev, base + 4), p5 = __shfl_sync(0xffffffffu, prev, base + 5);
-    if (has) {
-      const double* M = sub == 0 ? U + 36 * (k - 1) + 6 * r : U + 36 * k + 6 * r;
-      part = M[0] * p0 + M[1] * p1 + M[2] * p2 + M[3] * p3 + M[4] * p4 + M[5] * p5;
+    double t[6];
+    double bk[6];
+    ld6(b + 6 * k, bk);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      double o = __shfl_xor_sync(0xffffffffu, part[r], 1);
+      double pt = top ? part[r] : o, pb = top ? o : part[r];
+      t[r] = bk[r] - (pt + pb);
     }
+    double Dk[36];
+    ld36(D + 36 * k, Dk);
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+      xk[r] = Dk[6 * r] * t[0] + Dk[6 * r + 1] * t[1] + Dk[6 * r + 2] * t[2] + Dk[6 * r + 3] * t[3] +
+              Dk[6 * r + 4] * t[4] + Dk[6 * r + 5] * t[5];
   }
-  const double opart = __shfl_sync(0xffffffffu, part, other + r);
-  const double ptop = sub == 0 ? part : opart, pbot = sub == 0 ? opart : part;
-  const double tk = b[6 * k + r] - (ptop + pbot);
-  double xk;
-  {
-    const double* Dk = D + 36 * k + 6 * r;
-    double q0 = __shfl_sync(0xffffffffu, tk, base + 0), q1 = __shfl_sync(0xffffffffu, tk, base + 1);
-    double q2 = __shfl_sync(0xffffffffu, tk, base + 2), q3 = __shfl_sync(0xffffffffu, tk, base + 3);
-    double q4 = __shfl_sync(0xffffffffu, tk, base + 4), q5 = __shfl_sync(0xffffffffu, tk, base + 5);
-    xk = Dk[0] * q0 + Dk[1] * q1 + Dk[2] * q2 + Dk[3] * q3 + Dk[4] * q4 + Dk[5] * q5;
+  __syncwarp();
+  // z_i = Dinv_i v_i for every block but k, all lanes
+  const int nb = nrhs * N;
+  for (int q = lane; q < nb; q += 32) {
+    const int gg = q / N, i = q - gg * N;
+    if (i == k) continue;
+    double* vi = tmp + gg * stride + 6 * i;
+    double vv[6], Dm[36], z[6];
+    ld6(vi, vv);
+    ld36(D + 36 * i, Dm);
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+      z[r] = Dm[6 * r] * vv[0] + Dm[6 * r + 1] * vv[1] + Dm[6 * r + 2] * vv[2] + Dm[6 * r + 3] * vv[3] +
+             Dm[6 * r + 4] * vv[4] + Dm[6 * r + 5] * vv[5];
+    st6(vi, z);
   }
-  __syncwarp();  // sweep-1 values visible; b fully consumed (out may alias rhs)
-  if (act && sub == 0) x[6 * k + r] = xk;
-  // sweep 2: top i = k-1..0 (x_i = Sinv_i v_i - X_{i+1}^T x_{i+1}); bottom i = k+1..N-1
-  double xp = xk;
-  for (int t = 0; t < steps; ++t) {
-    const bool live = t < my_n;
-    const int i = sub == 0 ? k - 1 - t : k + 1 + t;
-    double dv = 0.0;
-    if (live) {
-      const double* Di = D + 36 * i + 6 * r;
-      const double* vi = v + 6 * i;
-      dv = Di[0] * vi[0] + Di[1] * vi[1] + Di[2] * vi[2] + Di[3] * vi[3] + Di[4] * vi[4] + Di[5] * vi[5];
-    }
-    double p0 = __shfl_sync(0xffffffffu, xp, base + 0), p1 = __shfl_sync(0xffffffffu, xp, base + 1);
-    double p2 = __shfl_sync(0xffffffffu, xp, base + 2), p3 = __shfl_sync(0xffffffffu, xp, base + 3);
-    double p4 = __shfl_sync(0xffffffffu, xp, base + 4), p5 = __shfl_sync(0xffffffffu, xp, base + 5);
-    if (live) {
-      const double* Mc = sub == 0 ? U + 36 * i + r : U + 36 * (i - 1) + r;  // column r of X_{i+1} / Y_{i-1}
-      double a1 = Mc[6] * p1 + Mc[18] * p3 + Mc[30] * p5;
-      xp = dv - (Mc[0] * p0 + Mc[12] * p2 + Mc[24] * p4 + a1);
-      if (act) x[6 * i + r] = xp;
+  __syncwarp();
+  if (act) {
+    if (top) st6(x + 6 * k, xk);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) p[r] = xk[r];
+    for (int t = 0; t < cnt; ++t) {
+      const int i = top ? k - 1 - t : k + 1 + t;
+      double a[6], M[36];
+      ld6(v + 6 * i, a);
+      ld36(top ? U + 36 * i : U + 36 * (i - 1), M);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        double s0 = M[r] * p[0] + M[12 + r] * p[2] + M[24 + r] * p[4];
+        double s1 = M[6 + r] * p[1] + M[18 + r] * p[3] + M[30 + r] * p[5];
+        a[r] -= s0 + s1;
+      }
+#pragma unroll
+      for (int r = 0; r < 6; ++r) p[r] = a[r];
+      st6(x + 6 * i, a);
     }
   }
   __syncwarp();

@@ -104,11 +104,14 @@ DEV int element_pass(const Team& team, const Problem& P, const double* x, Ws& ws
     d[7] = d[8] = 0.0;
     // f_loc = K_local d, rotated per 3-block by the frame   (beam.py:311-325)
     double fl[12];
+#pragma unroll
     for (int i = 0; i < 12; ++i) {
       double acc = 0.0;
+#pragma unroll
       for (int j = 3; j < 12; ++j) acc += d[j] * M.kl[12 * i + j];
       fl[i] = acc;
     }
+#pragma unroll
     for (int b = 0; b < 4; ++b) mat3_vec(F, fl + 3 * b, ws.fe + 12 * e + 3 * b);
     if (tangent) {
       // 3x3 blocks B_pq = F kl_pq F^T of the element matrix, symmetrised

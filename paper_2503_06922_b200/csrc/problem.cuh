@@ -86,7 +86,7 @@ struct Ws {
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
 };
 
-constexpr int kMultiRhs = 2;  // right-hand sides solved concurrently by one warp (12 lanes each)
+constexpr int kMultiRhs = 16;  // right-hand sides solved concurrently by one warp (2 lanes each)
 
 // Carve a team's workspace.  Arrays touched by every ADMM iteration (the
 // factor, the scaled iterate and the row state) come from `hot` (shared

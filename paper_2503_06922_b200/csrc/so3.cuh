@@ -54,17 +54,26 @@ DEV void quat_from_matrix(const double* m, double* q) {
   if (m[4] > best) { best = m[4]; ch = 1; }
   if (m[8] > best) { best = m[8]; ch = 2; }
   if (tr > best) { ch = 3; }
-  if (ch == 3) {
+  if (ch == 0) {
+    q[0] = 1.0 - tr + 2.0 * m[0];
+    q[1] = m[3] + m[1];
+    q[2] = m[6] + m[2];
+    q[3] = m[7] - m[5];
+  } else if (ch == 1) {
+    q[1] = 1.0 - tr + 2.0 * m[4];
+    q[2] = m[7] + m[5];
+    q[0] = m[1] + m[3];
+    q[3] = m[2] - m[6];
+  } else if (ch == 2) {
+    q[2] = 1.0 - tr + 2.0 * m[8];
+    q[0] = m[2] + m[6];
+    q[1] = m[5] + m[7];
+    q[3] = m[3] - m[1];
+  } else {
     q[0] = m[7] - m[5];
     q[1] = m[2] - m[6];
     q[2] = m[3] - m[1];
     q[3] = 1.0 + tr;
-  } else {
-    int i = ch, j = (i + 1) % 3, k = (j + 1) % 3;
-    q[i] = 1.0 - tr + 2.0 * m[4 * i];
-    q[j] = m[3 * j + i] + m[3 * i + j];
-    q[k] = m[3 * k + i] + m[3 * i + k];
-    q[3] = m[3 * k + j] - m[3 * j + k];
   }
   quat_normalize(q);
 }

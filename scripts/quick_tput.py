@@ -10,7 +10,8 @@ eng = Engine(**w.engine_kwargs(), device=0)
 t = lambda a: torch.tensor(a, device="cuda:0")
 x0, ten, app = t(w.x0), t(w.tensions), t(w.applied)
 print("teams resident", eng._lib.accfem_teams_resident(eng._h))
-for rep in range(3):
+REPS = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+for rep in range(REPS):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     r = eng.solve_static_batch(x0, ten, app, tol=w.tol, max_frames=w.max_frames)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
