@@ -66,98 +66,153 @@ DEV bool spd6_inv(const double* S, double* Inv) {
 
 DEV int twist_split(int N) { return (N - 1) / 2; }
 
-// In-place twisted factorisation.  scratch: 4 x 36 doubles per team.
+// Diagonal blocks are symmetric and stored packed: 21 lower entries padded to
+// kDiag doubles so every block starts 16-byte aligned.
+constexpr int kDiag = 22;
+DEV int sidx(int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; }
+DEV void unpack_sym(const double* p, double* a) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) a[6 * r + c] = p[sidx(r, c)];
+}
+DEV void pack_sym(double* p, const double* a) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) p[r * (r + 1) / 2 + c] = a[6 * r + c];
+}
+
+// 6x6 / 6-vector register loads (16-byte aligned pointers)
+DEV void ld36(const double* p, double* a) {
+#if defined(__CUDA_ARCH__)
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 18; ++i) {
+    double2 v = q[i];
+    a[2 * i] = v.x;
+    a[2 * i + 1] = v.y;
+  }
+#else
+  for (int i = 0; i < 36; ++i) a[i] = p[i];
+#endif
+}
+DEV void st36(double* p, const double* a) {
+#if defined(__CUDA_ARCH__)
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 18; ++i) q[i] = make_double2(a[2 * i], a[2 * i + 1]);
+#else
+  for (int i = 0; i < 36; ++i) p[i] = a[i];
+#endif
+}
+DEV void ld6(const double* p, double* a) {
+#if defined(__CUDA_ARCH__)
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double2 v = q[i];
+    a[2 * i] = v.x;
+    a[2 * i + 1] = v.y;
+  }
+#else
+  for (int i = 0; i < 6; ++i) a[i] = p[i];
+#endif
+}
+DEV void st6(double* p, const double* a) {
+#if defined(__CUDA_ARCH__)
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) q[i] = make_double2(a[2 * i], a[2 * i + 1]);
+#else
+  for (int i = 0; i < 6; ++i) p[i] = a[i];
+#endif
+}
+
+// In-place twisted factorisation (D packed, kDiag per block; U full 6x6).
 // Returns the block of a failed pivot, or -1.
+DEV bool schur_block(bool top, const double* Ap, const double* C, const double* P, double* Xout, double* Dout) {
+  double X[36], S[36];
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a += (top ? C[6 * q + r] : C[6 * r + q]) * P[6 * q + c];
+      X[6 * r + c] = a;
+    }
+  unpack_sym(Ap, S);
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double a = S[6 * r + c];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * (top ? C[6 * q + c] : C[6 * c + q]);
+      S[6 * r + c] = a;
+    }
+  st36(Xout, X);
+  double Inv[36];
+  bool ok = spd6_inv(S, Inv);
+  pack_sym(Dout, Inv);
+  return ok;
+}
+
 DEV int twisted_factor(const TeamSerial&, int N, double* D, double* U, double* scratch) {
   const int k = twist_split(N);
-  double Sinv[36], X[36], Sn[36];
-  // top: blocks 0..k-1
-  for (int i = 0; i < k; ++i) {
-    for (int t = 0; t < 36; ++t) Sn[t] = D[36 * i + t];
-    if (i > 0) {
-      const double* C = U + 36 * (i - 1);
-      // X = C^T Sinv_{i-1};  S = A - X C
+  int fail = -1;
+  for (int half = 0; half < 2; ++half) {
+    const bool top = half == 0;
+    const int cnt = top ? k : N - 1 - k;
+    for (int t = 0; t < cnt; ++t) {
+      const int i = top ? t : N - 1 - t;
+      bool ok;
+      if (t == 0) {
+        double S[36], Inv[36];
+        unpack_sym(D + kDiag * i, S);
+        ok = spd6_inv(S, Inv);
+        pack_sym(D + kDiag * i, Inv);
+      } else {
+        double C[36], P[36];
+        double* Cp = top ? U + 36 * (i - 1) : U + 36 * i;
+        for (int e = 0; e < 36; ++e) C[e] = Cp[e];
+        unpack_sym(top ? D + kDiag * (i - 1) : D + kDiag * (i + 1), P);
+        ok = schur_block(top, D + kDiag * i, C, P, Cp, D + kDiag * i);
+      }
+      if (!ok && fail < 0) fail = i;
+    }
+    // middle contribution of this half
+    double part[36];
+    for (int e = 0; e < 36; ++e) part[e] = 0.0;
+    if (cnt > 0) {
+      double C[36], P[36], X[36];
+      double* Cp = top ? U + 36 * (k - 1) : U + 36 * k;
+      for (int e = 0; e < 36; ++e) C[e] = Cp[e];
+      unpack_sym(top ? D + kDiag * (k - 1) : D + kDiag * (k + 1), P);
       for (int r = 0; r < 6; ++r)
         for (int c = 0; c < 6; ++c) {
           double a = 0.0;
-          for (int q = 0; q < 6; ++q) a += C[6 * q + r] * Sinv[6 * q + c];
+          for (int q = 0; q < 6; ++q) a += (top ? C[6 * q + r] : C[6 * r + q]) * P[6 * q + c];
           X[6 * r + c] = a;
         }
-      for (int r = 0; r < 6; ++r)
-        for (int c = 0; c < 6; ++c) {
-          double a = Sn[6 * r + c];
-          for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * C[6 * q + c];
-          Sn[6 * r + c] = a;
-        }
-      for (int t = 0; t < 36; ++t) U[36 * (i - 1) + t] = X[t];
-    }
-    if (!spd6_inv(Sn, Sinv)) return i;
-    for (int t = 0; t < 36; ++t) D[36 * i + t] = Sinv[t];
-  }
-  // bottom: blocks N-1 .. k+1
-  for (int i = N - 1; i > k; --i) {
-    for (int t = 0; t < 36; ++t) Sn[t] = D[36 * i + t];
-    if (i < N - 1) {
-      const double* C = U + 36 * i;
-      const double* Tn = D + 36 * (i + 1);
-      // Y = C Tinv_{i+1};  T = A - Y C^T
+      for (int e = 0; e < 36; ++e) Cp[e] = X[e];
       for (int r = 0; r < 6; ++r)
         for (int c = 0; c < 6; ++c) {
           double a = 0.0;
-          for (int q = 0; q < 6; ++q) a += C[6 * r + q] * Tn[6 * q + c];
-          X[6 * r + c] = a;
+          for (int q = 0; q < 6; ++q) a += X[6 * r + q] * (top ? C[6 * q + c] : C[6 * c + q]);
+          part[6 * r + c] = a;
         }
-      for (int r = 0; r < 6; ++r)
-        for (int c = 0; c < 6; ++c) {
-          double a = Sn[6 * r + c];
-          for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * C[6 * c + q];
-          Sn[6 * r + c] = a;
-        }
-      for (int t = 0; t < 36; ++t) U[36 * i + t] = X[t];
     }
-    if (!spd6_inv(Sn, Sinv)) return i;
-    for (int t = 0; t < 36; ++t) D[36 * i + t] = Sinv[t];
+    for (int e = 0; e < 36; ++e) scratch[36 * half + e] = part[e];
   }
-  // middle
-  for (int t = 0; t < 36; ++t) Sn[t] = D[36 * k + t];
-  if (k > 0) {
-    const double* C = U + 36 * (k - 1);
-    const double* Sp = D + 36 * (k - 1);
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
-        double a = 0.0;
-        for (int q = 0; q < 6; ++q) a += C[6 * q + r] * Sp[6 * q + c];
-        X[6 * r + c] = a;
-      }
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
-        double a = Sn[6 * r + c];
-        for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * C[6 * q + c];
-        Sn[6 * r + c] = a;
-      }
-    for (int t = 0; t < 36; ++t) U[36 * (k - 1) + t] = X[t];
-  }
-  if (k < N - 1) {
-    const double* C = U + 36 * k;
-    const double* Tn = D + 36 * (k + 1);
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
-        double a = 0.0;
-        for (int q = 0; q < 6; ++q) a += C[6 * r + q] * Tn[6 * q + c];
-        X[6 * r + c] = a;
-      }
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
-        double a = Sn[6 * r + c];
-        for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * C[6 * c + q];
-        Sn[6 * r + c] = a;
-      }
-    for (int t = 0; t < 36; ++t) U[36 * k + t] = X[t];
-  }
-  if (!spd6_inv(Sn, Sinv)) return k;
-  for (int t = 0; t < 36; ++t) D[36 * k + t] = Sinv[t];
-  (void)scratch;
-  return -1;
+  double S[36], Inv[36];
+  unpack_sym(D + kDiag * k, S);
+  for (int e = 0; e < 36; ++e) S[e] = S[e] - (scratch[e] + scratch[36 + e]);
+  bool ok = spd6_inv(S, Inv);
+  pack_sym(D + kDiag * k, Inv);
+  if (!ok && fail < 0) fail = k;
+  return fail;
 }
 
 // Solve M x = r for `nrhs` right-hand sides: r_g = rhs + g*stride, result to
@@ -196,7 +251,7 @@ DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* 
     }
     for (int r = 0; r < 6; ++r) {
       double a = 0.0;
-      for (int j = 0; j < 6; ++j) a += D[36 * k + 6 * r + j] * t[j];
+      for (int j = 0; j < 6; ++j) a += D[kDiag * k + sidx(r, j)] * t[j];
       xk[r] = a;
     }
     // z_i = Dinv_i v_i (in place)
@@ -205,7 +260,7 @@ DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* 
       double z[6];
       for (int r = 0; r < 6; ++r) {
         double a = 0.0;
-        for (int j = 0; j < 6; ++j) a += D[36 * i + 6 * r + j] * v[6 * i + j];
+        for (int j = 0; j < 6; ++j) a += D[kDiag * i + sidx(r, j)] * v[6 * i + j];
         z[r] = a;
       }
       for (int r = 0; r < 6; ++r) v[6 * i + r] = z[r];
@@ -227,67 +282,12 @@ DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* 
   }
 }
 
+DEV void twisted_solve_multi(const TeamSerial& t, int N, const double* D, const double* U, const double* rhs,
+                             double* tmp, double* out, int nrhs, long stride) {
+  twisted_solve(t, N, D, U, rhs, tmp, out, nrhs, stride);
+}
+
 #if defined(__CUDACC__)
-// 6x6 helpers on register arrays
-DEV void ld36(const double* __restrict__ p, double* a) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-#pragma unroll
-  for (int i = 0; i < 18; ++i) {
-    double2 v = q[i];
-    a[2 * i] = v.x;
-    a[2 * i + 1] = v.y;
-  }
-}
-DEV void st36(double* p, const double* a) {
-  double2* q = reinterpret_cast<double2*>(p);
-#pragma unroll
-  for (int i = 0; i < 18; ++i) q[i] = make_double2(a[2 * i], a[2 * i + 1]);
-}
-DEV void ld6(const double* __restrict__ p, double* a) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    double2 v = q[i];
-    a[2 * i] = v.x;
-    a[2 * i + 1] = v.y;
-  }
-}
-DEV void st6(double* p, const double* a) {
-  double2* q = reinterpret_cast<double2*>(p);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) q[i] = make_double2(a[2 * i], a[2 * i + 1]);
-}
-
-// one Schur step on a single lane: X = C^T P (top) or C P (bottom), S = A - X C
-// (top) or A - X C^T (bottom); X written to Xout, inverse of S to Dout
-DEV bool schur_step(bool top, const double* A, const double* C, const double* P, double* Xout, double* Dout) {
-  double X[36], S[36];
-#pragma unroll
-  for (int r = 0; r < 6; ++r)
-#pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      double a = 0.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) a += (top ? C[6 * q + r] : C[6 * r + q]) * P[6 * q + c];
-      X[6 * r + c] = a;
-    }
-  st36(Xout, X);
-  ld36(A, S);
-#pragma unroll
-  for (int r = 0; r < 6; ++r)
-#pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      double a = S[6 * r + c];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) a -= X[6 * r + q] * (top ? C[6 * q + c] : C[6 * c + q]);
-      S[6 * r + c] = a;
-    }
-  double Inv[36];
-  bool ok = spd6_inv(S, Inv);
-  st36(Dout, Inv);
-  return ok;
-}
-
 // Warp factorisation: lane 0 runs the top recursion, lane 1 the bottom one,
 // each 6x6 step entirely in registers; they meet at the middle block.
 DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double* scratch) {
@@ -302,19 +302,18 @@ DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double
       bool ok;
       if (t == 0) {
         double S[36], Inv[36];
-        ld36(D + 36 * i, S);
+        unpack_sym(D + kDiag * i, S);
         ok = spd6_inv(S, Inv);
-        st36(D + 36 * i, Inv);
+        pack_sym(D + kDiag * i, Inv);
       } else {
         double C[36], P[36];
         double* Cp = top ? U + 36 * (i - 1) : U + 36 * i;
         ld36(Cp, C);
-        ld36(top ? D + 36 * (i - 1) : D + 36 * (i + 1), P);
-        ok = schur_step(top, D + 36 * i, C, P, Cp, D + 36 * i);
+        unpack_sym(top ? D + kDiag * (i - 1) : D + kDiag * (i + 1), P);
+        ok = schur_block(top, D + kDiag * i, C, P, Cp, D + kDiag * i);
       }
       if (!ok && fail == (1 << 30)) fail = i;
     }
-    // middle contributions X_k C_{k-1} (top) and Y_k C_k^T (bottom)
     double part[36];
 #pragma unroll
     for (int e = 0; e < 36; ++e) part[e] = 0.0;
@@ -322,7 +321,7 @@ DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double
       double C[36], P[36], X[36];
       double* Cp = top ? U + 36 * (k - 1) : U + 36 * k;
       ld36(Cp, C);
-      ld36(top ? D + 36 * (k - 1) : D + 36 * (k + 1), P);
+      unpack_sym(top ? D + kDiag * (k - 1) : D + kDiag * (k + 1), P);
 #pragma unroll
       for (int r = 0; r < 6; ++r)
 #pragma unroll
@@ -348,13 +347,13 @@ DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double
   __syncwarp();
   if (lane == 0) {
     double S[36], Pt[36], Pb[36], Inv[36];
-    ld36(D + 36 * k, S);
+    unpack_sym(D + kDiag * k, S);
     ld36(scratch, Pt);
     ld36(scratch + 36, Pb);
 #pragma unroll
     for (int e = 0; e < 36; ++e) S[e] = S[e] - (Pt[e] + Pb[e]);
     bool ok = spd6_inv(S, Inv);
-    st36(D + 36 * k, Inv);
+    pack_sym(D + kDiag * k, Inv);
     if (!ok && fail == (1 << 30)) fail = k;
   }
   __syncwarp();
@@ -362,12 +361,103 @@ DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double
   return worst == (1 << 30) ? -1 : worst;
 }
 
-// Warp solve: right-hand side g (< 16) is swept by lanes 2g (top half) and
-// 2g+1 (bottom half); each step is a full 6x6 mat-vec in one lane's
-// registers, so the recurrence carries no shuffles.  The independent
-// z_i = Dinv_i v_i products run across all lanes between the sweeps.
+// Single-RHS warp solve: lanes 0-5 sweep the top half, lanes 6-11 the bottom
+// half, lane row r = lane % 6; each step is one 6-wide shuffle mat-vec whose
+// operand loads are issued before the shuffles.  out may alias rhs, not tmp.
 DEV void twisted_solve(const TeamWarp& team, int N, const double* __restrict__ D, const double* __restrict__ U,
                        const double* rhs, double* tmp, double* out, int nrhs, long stride) {
+  (void)nrhs;
+  (void)stride;
+  const int lane = team.lane;
+  const int sub = lane < 6 ? 0 : (lane < 12 ? 1 : 2);  // lanes >= 12 shadow the top half
+  const int r = lane % 6;
+  const bool act = sub < 2;
+  const bool top = sub != 1;
+  const int base = top ? 0 : 6;
+  const int k = twist_split(N);
+  const int my_n = top ? k : N - 1 - k;
+  const int steps = (N - 1 - k) > k ? (N - 1 - k) : k;
+  double prev = 0.0;
+  for (int t = 0; t < steps; ++t) {
+    const bool live = t < my_n;
+    const int i = top ? t : N - 1 - t;
+    const double* M = top ? U + 36 * (i - 1) + 6 * r : U + 36 * i + 6 * r;
+    double a = 0.0, m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0, m5 = 0;
+    if (live) {
+      a = rhs[6 * i + r];
+      if (t > 0) {
+        m0 = M[0]; m1 = M[1]; m2 = M[2]; m3 = M[3]; m4 = M[4]; m5 = M[5];
+      }
+    }
+    if (t > 0) {
+      double p0 = __shfl_sync(0xffffffffu, prev, base + 0), p1 = __shfl_sync(0xffffffffu, prev, base + 1);
+      double p2 = __shfl_sync(0xffffffffu, prev, base + 2), p3 = __shfl_sync(0xffffffffu, prev, base + 3);
+      double p4 = __shfl_sync(0xffffffffu, prev, base + 4), p5 = __shfl_sync(0xffffffffu, prev, base + 5);
+      a -= (m0 * p0 + m2 * p2 + m4 * p4) + (m1 * p1 + m3 * p3 + m5 * p5);
+    }
+    if (live) {
+      prev = a;
+      if (act) tmp[6 * i + r] = a;
+    }
+  }
+  // middle: x_k = Zinv (b_k - (X_k v_{k-1} + Y_k u_{k+1}))
+  double part = 0.0;
+  {
+    const double* M = top ? U + 36 * (k - 1) + 6 * r : U + 36 * k + 6 * r;
+    double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0, m5 = 0;
+    if (my_n > 0) {
+      m0 = M[0]; m1 = M[1]; m2 = M[2]; m3 = M[3]; m4 = M[4]; m5 = M[5];
+    }
+    double p0 = __shfl_sync(0xffffffffu, prev, base + 0), p1 = __shfl_sync(0xffffffffu, prev, base + 1);
+    double p2 = __shfl_sync(0xffffffffu, prev, base + 2), p3 = __shfl_sync(0xffffffffu, prev, base + 3);
+    double p4 = __shfl_sync(0xffffffffu, prev, base + 4), p5 = __shfl_sync(0xffffffffu, prev, base + 5);
+    part = m0 * p0 + m1 * p1 + m2 * p2 + m3 * p3 + m4 * p4 + m5 * p5;
+  }
+  const double opart = __shfl_sync(0xffffffffu, part, (top ? 6 : 0) + r);
+  const double tk = rhs[6 * k + r] - ((top ? part : opart) + (top ? opart : part));
+  double xk;
+  {
+    const double* Dk = D + kDiag * k;
+    double d0 = Dk[sidx(r, 0)], d1 = Dk[sidx(r, 1)], d2 = Dk[sidx(r, 2)];
+    double d3 = Dk[sidx(r, 3)], d4 = Dk[sidx(r, 4)], d5 = Dk[sidx(r, 5)];
+    double q0 = __shfl_sync(0xffffffffu, tk, base + 0), q1 = __shfl_sync(0xffffffffu, tk, base + 1);
+    double q2 = __shfl_sync(0xffffffffu, tk, base + 2), q3 = __shfl_sync(0xffffffffu, tk, base + 3);
+    double q4 = __shfl_sync(0xffffffffu, tk, base + 4), q5 = __shfl_sync(0xffffffffu, tk, base + 5);
+    xk = (d0 * q0 + d2 * q2 + d4 * q4) + (d1 * q1 + d3 * q3 + d5 * q5);
+  }
+  __syncwarp();  // sweep-1 values visible; rhs fully consumed (out may alias rhs)
+  if (sub == 0) out[6 * k + r] = xk;
+  // sweep 2: x_i = Dinv_i v_i - X_{i+1}^T x_{i+1} (top) / Dinv_i u_i - Y_{i-1}^T x_{i-1} (bottom)
+  double xp = xk;
+  for (int t = 0; t < steps; ++t) {
+    const bool live = t < my_n;
+    const int i = top ? k - 1 - t : k + 1 + t;
+    const double* Mc = top ? U + 36 * i + r : U + 36 * (i - 1) + r;  // column r
+    double dv = 0.0, m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0, m5 = 0;
+    if (live) {
+      const double* Di = D + kDiag * i;
+      const double* vi = tmp + 6 * i;
+      dv = (Di[sidx(r, 0)] * vi[0] + Di[sidx(r, 2)] * vi[2] + Di[sidx(r, 4)] * vi[4]) +
+           (Di[sidx(r, 1)] * vi[1] + Di[sidx(r, 3)] * vi[3] + Di[sidx(r, 5)] * vi[5]);
+      m0 = Mc[0]; m1 = Mc[6]; m2 = Mc[12]; m3 = Mc[18]; m4 = Mc[24]; m5 = Mc[30];
+    }
+    double p0 = __shfl_sync(0xffffffffu, xp, base + 0), p1 = __shfl_sync(0xffffffffu, xp, base + 1);
+    double p2 = __shfl_sync(0xffffffffu, xp, base + 2), p3 = __shfl_sync(0xffffffffu, xp, base + 3);
+    double p4 = __shfl_sync(0xffffffffu, xp, base + 4), p5 = __shfl_sync(0xffffffffu, xp, base + 5);
+    if (live) {
+      xp = dv - ((m0 * p0 + m2 * p2 + m4 * p4) + (m1 * p1 + m3 * p3 + m5 * p5));
+      if (act) out[6 * i + r] = xp;
+    }
+  }
+  __syncwarp();
+}
+
+// Many right-hand sides (g < 16): lanes 2g / 2g+1 sweep the top / bottom half
+// of RHS g with the full 6x6 mat-vec in registers; the z_i = Dinv_i v_i
+// products run across all lanes between the sweeps.  out may alias rhs.
+DEV void twisted_solve_multi(const TeamWarp& team, int N, const double* __restrict__ D,
+                             const double* __restrict__ U, const double* rhs, double* tmp, double* out, int nrhs,
+                             long stride) {
   const int lane = team.lane;
   const int g = lane >> 1;
   const bool top = (lane & 1) == 0;
@@ -398,7 +488,6 @@ DEV void twisted_solve(const TeamWarp& team, int N, const double* __restrict__ D
       st6(v + 6 * i, a);
     }
   }
-  // middle block: x_k = Zinv (b_k - (X_k v_{k-1} + Y_k u_{k+1}))
   double part[6] = {0, 0, 0, 0, 0, 0};
   if (act && cnt > 0) {
     double M[36];
@@ -410,8 +499,7 @@ DEV void twisted_solve(const TeamWarp& team, int N, const double* __restrict__ D
   }
   double xk[6];
   {
-    double t[6];
-    double bk[6];
+    double t[6], bk[6], Dk[36];
     ld6(b + 6 * k, bk);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
@@ -419,15 +507,13 @@ DEV void twisted_solve(const TeamWarp& team, int N, const double* __restrict__ D
       double pt = top ? part[r] : o, pb = top ? o : part[r];
       t[r] = bk[r] - (pt + pb);
     }
-    double Dk[36];
-    ld36(D + 36 * k, Dk);
+    unpack_sym(D + kDiag * k, Dk);
 #pragma unroll
     for (int r = 0; r < 6; ++r)
       xk[r] = Dk[6 * r] * t[0] + Dk[6 * r + 1] * t[1] + Dk[6 * r + 2] * t[2] + Dk[6 * r + 3] * t[3] +
               Dk[6 * r + 4] * t[4] + Dk[6 * r + 5] * t[5];
   }
   __syncwarp();
-  // z_i = Dinv_i v_i for every block but k, all lanes
   const int nb = nrhs * N;
   for (int q = lane; q < nb; q += 32) {
     const int gg = q / N, i = q - gg * N;
@@ -435,7 +521,7 @@ DEV void twisted_solve(const TeamWarp& team, int N, const double* __restrict__ D
     double* vi = tmp + gg * stride + 6 * i;
     double vv[6], Dm[36], z[6];
     ld6(vi, vv);
-    ld36(D + 36 * i, Dm);
+    unpack_sym(D + kDiag * i, Dm);
 #pragma unroll
     for (int r = 0; r < 6; ++r)
       z[r] = Dm[6 * r] * vv[0] + Dm[6 * r + 1] * vv[1] + Dm[6 * r + 2] * vv[2] + Dm[6 * r + 3] * vv[3] +

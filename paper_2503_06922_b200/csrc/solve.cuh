@@ -89,11 +89,41 @@ DEV double col_dot(const Problem& P, const Frame& F, const Ws& ws, int j, const 
 // (solver.py:169-212).  Produces HD/HU (scaled H), as (scaled rows), gs, d,
 // e and returns c.
 // ---------------------------------------------------------------------------
+// packed (r, c) of entry p < 21 of a symmetric 6x6 block
+DEV void sym_rc(int p, int& r, int& c) {
+  r = p < 1 ? 0 : p < 3 ? 1 : p < 6 ? 2 : p < 10 ? 3 : p < 15 ? 4 : 5;
+  c = p - r * (r + 1) / 2;
+}
+
+// column infinity-norm of the block-tridiagonal H at DOF j (packed diagonal blocks)
+DEV double hcol_max(const double* HD, const double* HU, int N, int j) {
+  const int k = j / 6, cc = j % 6;
+  double mx = 0.0;
+  const double* dk = HD + kDiag * k;
+#pragma unroll
+  for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(dk[sidx(r, cc)]));
+  if (k + 1 < N) {
+    const double* u = HU + 36 * k + 6 * cc;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(u[r]));
+  }
+  if (k > 0) {
+    const double* u = HU + 36 * (k - 1) + cc;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(u[6 * r]));
+  }
+  return mx;
+}
+
 template <class Team>
 DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   const int N = P.m.N, n = 6 * N, E = N - 1;
   const int nf = F.nf, m = F.m;
-  PARFOR(i, 36 * N) ws.HD[i] = ws.KD[i];
+  PARFOR(i, 21 * N) {
+    int k = i / 21, p = i - 21 * k, r, c;
+    sym_rc(p, r, c);
+    ws.HD[kDiag * k + p] = ws.KD[36 * k + 6 * r + c];
+  }
   PARFOR(i, 36 * E) ws.HU[i] = ws.KU[i];
   PARFOR(j, n) {
     ws.gs[j] = ws.g[j];
@@ -116,17 +146,12 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   double* ee = ws.tr;
   for (int sweep = 0; sweep < P.s.scaling_iterations; ++sweep) {
     PARFOR(j, n) {
-      int k = j / 6, cc = j % 6;
-      double mx = 0.0;
-      for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HD[36 * k + 6 * r + cc]));
-      if (k + 1 < N)
-        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * k + 6 * cc + r]));
-      if (k > 0)
-        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * (k - 1) + 6 * r + cc]));
+      double mx = hcol_max(ws.HD, ws.HU, N, j);
       int fr = P.m.fixed_row_of_dof[j];
       if (fr >= 0) mx = fmax(mx, fabs(ws.as[3 * fr]));
+      int cc = j % 6;
       if (cc < 3) {
-        int ct = ws.crow_of_node[k];
+        int ct = ws.crow_of_node[j / 6];
         if (ct >= 0) mx = fmax(mx, fabs(ws.as[3 * (nf + ct) + cc]));
       }
       dd[j] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
@@ -137,12 +162,13 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
       ee[r] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
     }
     team.sync();
-    PARFOR(i, 36 * N) {
-      int k = i / 36, r = (i % 36) / 6, cc = i % 6;
-      ws.HD[i] *= dd[6 * k + r] * dd[6 * k + cc];
+    PARFOR(i, 21 * N) {
+      int k = i / 21, p = i - 21 * k, r, cc;
+      sym_rc(p, r, cc);
+      ws.HD[kDiag * k + p] *= dd[6 * k + r] * dd[6 * k + cc];
     }
     PARFOR(i, 36 * E) {
-      int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+      int k = i / 36, t = i - 36 * k, r = t / 6, cc = t - 6 * r;
       ws.HU[i] *= dd[6 * k + r] * dd[6 * (k + 1) + cc];
     }
     PARFOR(r, m) {
@@ -162,20 +188,16 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
     // cost normalisation: column maxima of the scaled H only
     double csum = 0.0, gmax = 0.0;
     PARFOR(j, n) {
-      int k = j / 6, cc = j % 6;
-      double mx = 0.0;
-      for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HD[36 * k + 6 * r + cc]));
-      if (k + 1 < N)
-        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * k + 6 * cc + r]));
-      if (k > 0)
-        for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(ws.HU[36 * (k - 1) + 6 * r + cc]));
-      csum += mx;
+      csum += hcol_max(ws.HD, ws.HU, N, j);
       gmax = fmax(gmax, fabs(ws.gs[j]));
     }
     csum = team.sum(csum);
     gmax = team.max(gmax);
     double gam = 1.0 / fmax(fmax(csum / n, gmax), 1e-12);
-    PARFOR(i, 36 * N) ws.HD[i] *= gam;
+    PARFOR(i, 21 * N) {
+      int k = i / 21;
+      ws.HD[kDiag * k + (i - 21 * k)] *= gam;
+    }
     PARFOR(i, 36 * E) ws.HU[i] *= gam;
     PARFOR(j, n) ws.gs[j] *= gam;
     c *= gam;
@@ -261,16 +283,17 @@ template <class Team>
 DEV int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws) {
   const int N = P.m.N, E = N - 1;
   const int* frd = P.m.fixed_row_of_dof;
-  PARFOR(i, 36 * N) {
-    int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+  PARFOR(i, 21 * N) {
+    int k = i / 21, p = i - 21 * k, r, cc;
+    sym_rc(p, r, cc);
     bool fr = frd[6 * k + r] >= 0, fc = frd[6 * k + cc] >= 0;
-    double v = ws.KD[i];
+    double v = ws.KD[36 * k + 6 * r + cc];
     if (fr || fc) v = (r == cc) ? 1.0 : 0.0;
     else if (r == cc) v += delta;
-    ws.HD[i] = v;
+    ws.HD[kDiag * k + p] = v;
   }
   PARFOR(i, 36 * E) {
-    int k = i / 36, r = (i % 36) / 6, cc = i % 6;
+    int k = i / 36, t = i - 36 * k, r = t / 6, cc = t - 6 * r;
     bool fr = frd[6 * k + r] >= 0, fc = frd[6 * (k + 1) + cc] >= 0;
     ws.HU[i] = (fr || fc) ? 0.0 : ws.KU[i];
   }
@@ -480,7 +503,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
         }
       }
       team.sync();
-      twisted_solve(team, N, ws.HD, ws.HU, ws.Wc, ws.Wc + kMultiRhs * n, ws.Wc, nb, n);
+      twisted_solve_multi(team, N, ws.HD, ws.HU, ws.Wc, ws.Wc + kMultiRhs * n, ws.Wc, nb, n);
       team.sync();
       PARFOR(t, na * nb) {
         int p = t / nb, b = t % nb;
@@ -614,10 +637,11 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     ws.us[r] = ws.e[r] * ws.up[r];
   }
   team.sync();
-  // M = H_s + sigma I + A_s^T diag(rho) A_s  (into HD; HU already holds H_s off-diagonal)
-  PARFOR(i, 36 * N) {
-    int k = i / 36, r = (i % 36) / 6, cc = i % 6;
-    double v = ws.HD[i];
+  // M = H_s + sigma I + A_s^T diag(rho) A_s  (packed diagonal blocks; HU holds H_s off-diagonal)
+  PARFOR(i, 21 * N) {
+    int k = i / 21, p = i - 21 * k, r, cc;
+    sym_rc(p, r, cc);
+    double v = ws.HD[kDiag * k + p];
     if (r == cc) {
       v += S.sigma;
       int fr = P.m.fixed_row_of_dof[6 * k + r];
@@ -630,7 +654,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
         v += ws.rho[row] * ws.as[3 * row + r] * ws.as[3 * row + cc];
       }
     }
-    ws.HD[i] = v;
+    ws.HD[kDiag * k + p] = v;
   }
   team.sync();
   PROF_T0(t_fac);
@@ -653,18 +677,22 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   bool infeas = false;
   PROF_T0(t_iter);
   for (k = 1; k <= S.max_iterations; ++k) {
-    PARFOR(r, m) ws.tr[r] = ws.rho[r] * (ws.z[r] - ws.y[r] / ws.rho[r]);
+    // rhs = sigma x - g_s + A_s^T (rho o (z - y / rho)); selector rows touch
+    // distinct DOFs, contact rows distinct nodes: two conflict-free passes
+    PARFOR(j, n) ws.rhs[j] = sg * ws.xs[j] - ws.gs[j];
     team.sync();
-    PARFOR(j, n) {
-      double v = sg * ws.xs[j] - ws.gs[j];
-      int fr = P.m.fixed_row_of_dof[j];
-      if (fr >= 0) v += ws.as[3 * fr] * ws.tr[fr];
-      int cc = j % 6;
-      if (cc < 3) {
-        int ct = ws.crow_of_node[j / 6];
-        if (ct >= 0) v += ws.as[3 * (nf + ct) + cc] * ws.tr[nf + ct];
-      }
-      ws.rhs[j] = v;
+    PARFOR(r, nf) {
+      double t = ws.rho[r] * (ws.z[r] - ws.y[r] / ws.rho[r]);
+      ws.rhs[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]] += ws.as[3 * r] * t;
+    }
+    team.sync();
+    PARFOR(c, m - nf) {
+      int r = nf + c;
+      double t = ws.rho[r] * (ws.z[r] - ws.y[r] / ws.rho[r]);
+      double* rr = ws.rhs + 6 * ws.cnode[c];
+      rr[0] += ws.as[3 * r] * t;
+      rr[1] += ws.as[3 * r + 1] * t;
+      rr[2] += ws.as[3 * r + 2] * t;
     }
     team.sync();
     PROF_T0(t_ch);
