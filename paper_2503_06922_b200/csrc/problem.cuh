@@ -84,6 +84,7 @@ struct Ws {
   double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr;
   int *act, *alist;
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
+  bool sh;                   // hot arrays live in shared memory
 };
 
 constexpr int kMultiRhs = 16;  // right-hand sides solved concurrently by one warp (2 lanes each)
@@ -131,6 +132,7 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   w.act = ip; ip = ip ? ip + m : nullptr;
   w.alist = ip;
   w.prof = nullptr;
+  w.sh = hot != nullptr;
   if (used) *used = off;
   if (hot_used) *hot_used = hot ? hoff : 0;
   return w;

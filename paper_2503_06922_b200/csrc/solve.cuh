@@ -298,7 +298,7 @@ DEV int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws)
     ws.HU[i] = (fr || fc) ? 0.0 : ws.KU[i];
   }
   team.sync();
-  return twisted_factor(team, N, ws.HD, ws.HU, ws.scr);
+  return twisted_factor(team, N, ws.HD, ws.HU, ws.scr, ws.sh);
 }
 
 // full-length rhs for the eliminated system: b at selector DOFs,
@@ -345,7 +345,7 @@ DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws,
   const int N = P.m.N, n = 6 * N;
   if (reduced_factor(team, P, 0.0, ws) >= 0) return ST_LINALG;
   eliminated_rhs(team, P, F, ws, ws.rhs);
-  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.dx, 1, 0);
+  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.dx, 1, 0, ws.sh);
   team.sync();
   for (int it = 0; it < 3; ++it) {
     block_matvec(team, N, ws.KD, ws.KU, ws.dx, ws.tmp);
@@ -354,7 +354,7 @@ DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws,
       ws.rhs[j] = fx ? 0.0 : -ws.g[j] - ws.tmp[j];
     }
     team.sync();
-    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0);
+    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0, ws.sh);
     team.sync();
     PARFOR(j, n) ws.dx[j] += ws.w[j];
     team.sync();
@@ -423,7 +423,7 @@ template <class Team>
 DEV void schur_solve(const Team& team, const Problem& P, Ws& ws, int na, const double* f, const double* h,
                      double* xo, double* yo) {
   const int N = P.m.N, n = 6 * N;
-  twisted_solve(team, N, ws.HD, ws.HU, f, ws.tmp, ws.v, 1, 0);
+  twisted_solve(team, N, ws.HD, ws.HU, f, ws.tmp, ws.v, 1, 0, ws.sh);
   team.sync();
   PARFOR(q, na) {
     int c = ws.alist[q];
@@ -445,7 +445,7 @@ DEV void schur_solve(const Team& team, const Problem& P, Ws& ws, int na, const d
     }
   }
   team.sync();
-  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0);
+  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0, ws.sh);
   team.sync();
   PARFOR(j, n) xo[j] = ws.v[j] - ws.w[j];
   team.sync();
@@ -658,7 +658,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   }
   team.sync();
   PROF_T0(t_fac);
-  int fbad = twisted_factor(team, N, ws.HD, ws.HU, ws.scr);
+  int fbad = twisted_factor(team, N, ws.HD, ws.HU, ws.scr, ws.sh);
   PROF_ADD(ws, PF_FACTOR, t_fac);
   if (fbad >= 0) return ST_LINALG;
   // initial iterate (solver.py:287-289)
@@ -696,7 +696,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     }
     team.sync();
     PROF_T0(t_ch);
-    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0);
+    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0, ws.sh);
     team.sync();
     PROF_ADD(ws, PF_CHAIN, t_ch);
     PARFOR(r, m) {
