@@ -220,8 +220,9 @@ DEV int twisted_factor(const TeamSerial&, int N, double* D, double* U, double* s
 // out + g*stride; tmp (same layout) holds the sweep-1 values.  out may alias
 // rhs or tmp.
 DEV void twisted_solve(const TeamSerial&, int N, const double* D, const double* U, const double* rhs, double* tmp,
-                       double* out, int nrhs, long stride, bool sh = false) {
+                       double* out, int nrhs, long stride, bool sh = false, bool shv = false) {
   (void)sh;
+  (void)shv;
   const int k = twist_split(N);
   for (int g = 0; g < nrhs; ++g) {
     const double* b = rhs + g * stride;
@@ -377,8 +378,18 @@ DEV int twisted_factor(const TeamWarp& team, int N, double* D, double* U, double
 // loops are branch-free (clamped addresses, predicated stores) and walk
 // incremental pointers; `sh` states that D and U live in shared memory.
 // out may alias rhs, not tmp.
+template <bool SH, bool SHV>
 DEV void twisted_solve_impl(const TeamWarp& team, int N, const double* __restrict__ D,
                             const double* __restrict__ U, const double* rhs, double* tmp, double* out) {
+  if (SH) {
+    __builtin_assume(__isShared(D));
+    __builtin_assume(__isShared(U));
+  }
+  if (SHV) {
+    __builtin_assume(__isShared(rhs));
+    __builtin_assume(__isShared(tmp));
+    __builtin_assume(__isShared(out));
+  }
   const int lane = team.lane;
   const int sub = lane < 6 ? 0 : (lane < 12 ? 1 : 2);  // lanes >= 12 shadow the top half
   const int r = lane % 6;
@@ -387,37 +398,40 @@ DEV void twisted_solve_impl(const TeamWarp& team, int N, const double* __restric
   const int base = top ? 0 : 6;
   const int k = twist_split(N);
   const int my_n = top ? k : N - 1 - k;
-  const int steps = (N - 1 - k) > k ? (N - 1 - k) : k;
-  // sweep 1
-  const long db = top ? 6 : -6;
-  const double* bp = rhs + (top ? 0 : 6L * (N - 1)) + r;
-  double* vp = tmp + (top ? 0 : 6L * (N - 1)) + r;
-  // coupling row r of step t >= 1: top X_t at U[t-1], bottom Y_{N-1-t} at U[N-1-t]
-  const long dM = top ? 36 : -36;
-  const double* Mp = (top ? U : U + 36L * (N - 2)) + 6 * r;
+  const int n_common = k < N - 1 - k ? k : N - 1 - k;
+  // ---- sweep 1: top v_t = b_t - X_t v_{t-1}; bottom u_i = b_i - Y_i u_{i+1}, i = N-1-t
+  const int db = top ? 6 : -6;
+  const int dM = top ? 36 : -36;
+  const double* bp = rhs + (top ? 0 : 6 * (N - 1)) + r;
+  double* vp = tmp + (top ? 0 : 6 * (N - 1)) + r;
+  const double* Mp = (top ? U : U + 36 * (N - 2)) + 6 * r;
   double prev = 0.0;
   if (my_n > 0) {
     prev = *bp;
     if (act) *vp = prev;
   }
-  for (int t = 1; t < steps; ++t) {
-    const bool live = t < my_n;
-    const long o = live ? (long)t * db : 0;
-    const long om = live ? (long)(t - 1) * dM : 0;
-    const double a0 = bp[o];
-    const double* M = Mp + om;
-    const double m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5];
+  auto step1 = [&](bool live) {
+    bp += db;
+    vp += db;
+    const double a0 = *bp;
+    const double m0 = Mp[0], m1 = Mp[1], m2 = Mp[2], m3 = Mp[3], m4 = Mp[4], m5 = Mp[5];
+    Mp += dM;
     const double p0 = __shfl_sync(0xffffffffu, prev, base + 0), p1 = __shfl_sync(0xffffffffu, prev, base + 1);
     const double p2 = __shfl_sync(0xffffffffu, prev, base + 2), p3 = __shfl_sync(0xffffffffu, prev, base + 3);
     const double p4 = __shfl_sync(0xffffffffu, prev, base + 4), p5 = __shfl_sync(0xffffffffu, prev, base + 5);
     const double a = a0 - ((m0 * p0 + m2 * p2 + m4 * p4) + (m1 * p1 + m3 * p3 + m5 * p5));
-    prev = live ? a : prev;
-    if (live && act) vp[o] = a;
-  }
-  // middle: x_k = Zinv (b_k - (X_k v_{k-1} + Y_k u_{k+1}))
+    if (live) {
+      prev = a;
+      if (act) *vp = a;
+    }
+  };
+  for (int t = 1; t < n_common; ++t) step1(true);
+  const int te = n_common > 1 ? n_common : 1;
+  if (k != N - 1 - k) step1(te < my_n);
+  // ---- middle: x_k = Zinv (b_k - (X_k v_{k-1} + Y_k u_{k+1}))
   double part;
   {
-    const double* M = (top ? U + 36L * (k > 0 ? k - 1 : 0) : U + 36L * (k < N - 1 ? k : 0)) + 6 * r;
+    const double* M = (top ? U + 36 * (k > 0 ? k - 1 : 0) : U + 36 * (k < N - 1 ? k : 0)) + 6 * r;
     const double m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5];
     const double p0 = __shfl_sync(0xffffffffu, prev, base + 0), p1 = __shfl_sync(0xffffffffu, prev, base + 1);
     const double p2 = __shfl_sync(0xffffffffu, prev, base + 2), p3 = __shfl_sync(0xffffffffu, prev, base + 3);
@@ -426,65 +440,70 @@ DEV void twisted_solve_impl(const TeamWarp& team, int N, const double* __restric
   }
   const double opart = __shfl_sync(0xffffffffu, part, (top ? 6 : 0) + r);
   const double tk = rhs[6 * k + r] - ((top ? part : opart) + (top ? opart : part));
-  // per-lane offsets of row r of a packed symmetric block
-  const int o0 = sidx(r, 0), o1 = sidx(r, 1), o2 = sidx(r, 2), o3 = sidx(r, 3), o4 = sidx(r, 4), o5 = sidx(r, 5);
   double xk;
   {
     const double* Dk = D + kDiag * k;
-    const double d0 = Dk[o0], d1 = Dk[o1], d2 = Dk[o2], d3 = Dk[o3], d4 = Dk[o4], d5 = Dk[o5];
+    const double d0 = Dk[sidx(r, 0)], d1 = Dk[sidx(r, 1)], d2 = Dk[sidx(r, 2)];
+    const double d3 = Dk[sidx(r, 3)], d4 = Dk[sidx(r, 4)], d5 = Dk[sidx(r, 5)];
     const double q0 = __shfl_sync(0xffffffffu, tk, base + 0), q1 = __shfl_sync(0xffffffffu, tk, base + 1);
     const double q2 = __shfl_sync(0xffffffffu, tk, base + 2), q3 = __shfl_sync(0xffffffffu, tk, base + 3);
     const double q4 = __shfl_sync(0xffffffffu, tk, base + 4), q5 = __shfl_sync(0xffffffffu, tk, base + 5);
     xk = (d0 * q0 + d2 * q2 + d4 * q4) + (d1 * q1 + d3 * q3 + d5 * q5);
   }
   __syncwarp();  // sweep-1 values visible; rhs fully consumed (out may alias rhs)
-  // z_i = Dinv_i v_i for every block but k, all lanes (lane handles row r of block i)
-  for (int q = lane; q < 6 * N; q += 32) {
-    const int i = q / 6, rr = q - 6 * i;
-    if (i == k) continue;
-    const double* Di = D + kDiag * i;
-    const double* vi = tmp + 6 * i;
-    const double z = (Di[sidx(rr, 0)] * vi[0] + Di[sidx(rr, 2)] * vi[2] + Di[sidx(rr, 4)] * vi[4]) +
-                     (Di[sidx(rr, 1)] * vi[1] + Di[sidx(rr, 3)] * vi[3] + Di[sidx(rr, 5)] * vi[5]);
-    out[q] = z;  // out != tmp: z parked in out, consumed below before x_i overwrites it
+  // ---- z_i = Dinv_i v_i for every block but k; lane handles (block, row) pairs
+  {
+    int i = lane / 6, rr = lane % 6;  // q = 6 i + rr, stepping by 32 = 5 blocks + 2 rows
+    for (int q = lane; q < 6 * N; q += 32) {
+      if (i != k) {
+        const double* Di = D + kDiag * i;
+        const double* vi = tmp + 6 * i;
+        const double z = (Di[sidx(rr, 0)] * vi[0] + Di[sidx(rr, 2)] * vi[2] + Di[sidx(rr, 4)] * vi[4]) +
+                         (Di[sidx(rr, 1)] * vi[1] + Di[sidx(rr, 3)] * vi[3] + Di[sidx(rr, 5)] * vi[5]);
+        out[q] = z;  // out != tmp: z parked in out, consumed below before x_i overwrites it
+      }
+      rr += 2;
+      i += 5;
+      if (rr >= 6) {
+        rr -= 6;
+        i += 1;
+      }
+    }
   }
   __syncwarp();
   if (sub == 0) out[6 * k + r] = xk;
-  // sweep 2: x_i = z_i - X_{i+1}^T x_{i+1} (top) / z_i - Y_{i-1}^T x_{i-1} (bottom)
+  // ---- sweep 2: top x_i = z_i - X_{i+1}^T x_{i+1}, i = k-1-t; bottom x_i = z_i - Y_{i-1}^T x_{i-1}, i = k+1+t
   double xp = xk;
-  const long dx = top ? -6 : 6;
-  double* xo = out + 6L * k + r;
-  // column r of step t: top X_{k-t} at U[k-1-t], bottom Y_{k+t} at U[k+t]
-  const long dC = top ? -36 : 36;
-  const double* Cp = (top ? U + 36L * (k > 0 ? k - 1 : 0) : U + 36L * (k < N - 1 ? k : 0)) + r;
-  for (int t = 0; t < steps; ++t) {
-    const bool live = t < my_n;
-    const long o = live ? (long)(t + 1) * dx : 0;
-    const long oc = live ? (long)t * dC : 0;
-    const double z = xo[o];
-    const double* Mc = Cp + oc;
-    const double m0 = Mc[0], m1 = Mc[6], m2 = Mc[12], m3 = Mc[18], m4 = Mc[24], m5 = Mc[30];
+  const int dx = top ? -6 : 6;
+  double* xo = out + 6 * k + r;
+  const int dC = top ? -36 : 36;
+  const double* Cp = (top ? U + 36 * (k > 0 ? k - 1 : 0) : U + 36 * (k < N - 1 ? k : 0)) + r;
+  auto step2 = [&](bool live) {
+    xo += dx;
+    const double z = *xo;
+    const double m0 = Cp[0], m1 = Cp[6], m2 = Cp[12], m3 = Cp[18], m4 = Cp[24], m5 = Cp[30];
+    Cp += dC;
     const double p0 = __shfl_sync(0xffffffffu, xp, base + 0), p1 = __shfl_sync(0xffffffffu, xp, base + 1);
     const double p2 = __shfl_sync(0xffffffffu, xp, base + 2), p3 = __shfl_sync(0xffffffffu, xp, base + 3);
     const double p4 = __shfl_sync(0xffffffffu, xp, base + 4), p5 = __shfl_sync(0xffffffffu, xp, base + 5);
     const double a = z - ((m0 * p0 + m2 * p2 + m4 * p4) + (m1 * p1 + m3 * p3 + m5 * p5));
-    xp = live ? a : xp;
-    if (live && act) xo[o] = a;
-  }
+    if (live) {
+      xp = a;
+      if (act) *xo = a;
+    }
+  };
+  for (int t = 0; t < n_common; ++t) step2(true);
+  if (k != N - 1 - k) step2(n_common < my_n);
   __syncwarp();
 }
 
 DEV void twisted_solve(const TeamWarp& team, int N, const double* D, const double* U, const double* rhs, double* tmp,
-                       double* out, int nrhs, long stride, bool sh = false) {
+                       double* out, int nrhs, long stride, bool sh = false, bool shv = false) {
   (void)nrhs;
   (void)stride;
-  if (sh) {
-    __builtin_assume(__isShared(D));
-    __builtin_assume(__isShared(U));
-    twisted_solve_impl(team, N, D, U, rhs, tmp, out);
-  } else {
-    twisted_solve_impl(team, N, D, U, rhs, tmp, out);
-  }
+  if (sh && shv) twisted_solve_impl<true, true>(team, N, D, U, rhs, tmp, out);
+  else if (sh) twisted_solve_impl<true, false>(team, N, D, U, rhs, tmp, out);
+  else twisted_solve_impl<false, false>(team, N, D, U, rhs, tmp, out);
 }
 
 // Many right-hand sides (g < 16): lanes 2g / 2g+1 sweep the top / bottom half

@@ -108,10 +108,9 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   };
   // hot: the factor (packed symmetric diagonal blocks, full couplings) and the solve vectors
   w.HD = takeh(22L * N); w.HU = takeh(36 * E);
-  w.rhs = takeh(n); w.tmp = takeh(n);
+  w.rhs = takeh(n); w.tmp = takeh(n); w.xs = takeh(n); w.gs = takeh(n);
   w.xt = w.rhs;  // the solve writes its result over the right-hand side
   // cold
-  w.xs = take(n); w.gs = take(n);
   w.z = take(m); w.y = take(m); w.yprev = take(m); w.rho = take(m); w.ls = take(m); w.us = take(m);
   w.tr = take(m); w.as = take(3 * m);
   w.R = take(9L * N); w.frames = take(9 * E); w.fe = take(12 * E); w.ke = take(108 * E);
@@ -149,7 +148,7 @@ HDEV long ws_hot_doubles(int N, int nf) {
   long n = 6L * N;
   (void)nf;
   auto r2 = [](long k) { return (k + 1) & ~1L; };
-  return r2(22L * N) + r2(36L * (N - 1)) + 2 * r2(n);
+  return r2(22L * N) + r2(36L * (N - 1)) + 4 * r2(n);
 }
 
 // ---------------------------------------------------------------------------

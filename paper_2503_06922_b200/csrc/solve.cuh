@@ -142,7 +142,7 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   }
   team.sync();
   double c = 1.0;
-  double* dd = ws.colh;
+  double* dd = ws.tmp;  // hot scratch: unused until the ADMM loop
   double* ee = ws.tr;
   for (int sweep = 0; sweep < P.s.scaling_iterations; ++sweep) {
     PARFOR(j, n) {
@@ -696,7 +696,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     }
     team.sync();
     PROF_T0(t_ch);
-    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0, ws.sh);
+    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0, ws.sh, ws.sh);
     team.sync();
     PROF_ADD(ws, PF_CHAIN, t_ch);
     PARFOR(r, m) {
