@@ -16,6 +16,7 @@ the CPU oracle consumes the same arrays scenario by scenario.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from functools import lru_cache
 
 import numpy as np
 
@@ -32,6 +33,7 @@ from .scene import (
 )
 
 CFG4_SEED = 20261018
+CFG4_TOTAL = 65536
 
 
 @dataclass
@@ -150,6 +152,22 @@ def cfg5(n_scenarios=1, target=200):
     return constriction(1001, target, "cfg5", n_scenarios)
 
 
+@lru_cache(maxsize=4)
+def _cfg4_table(seed, table):
+    """(tensions, load scale, insertion offset) of every scenario of the batch."""
+    l0 = 0.47 / 100
+    rng = np.random.default_rng(seed)
+    tensions = rng.uniform(0.0, 0.02, size=(table, 3))
+    scale = rng.uniform(1.0, 1.5, size=table)
+    offset = rng.uniform(0.0, 2.0 * l0, size=table)
+    return tensions, scale, offset
+
+
+@lru_cache(maxsize=1)
+def _cfg3_scene():
+    return cfg3(1)
+
+
 def cfg4(n_scenarios=65536, seed=CFG4_SEED, start=0):
     """Batch of cfg3 samples: T_j ~ U[0, 0.02] N, load scale ~ U[1, 1.5],
     insertion offset ~ U[0, 2 l0] along the lumen axis (encoded in x0).
@@ -158,14 +176,15 @@ def cfg4(n_scenarios=65536, seed=CFG4_SEED, start=0):
     shard [start, start + n) of the 65,536-scenario batch is reproducible on
     its own rank.
     """
-    base = cfg3(1)
+    base = _cfg3_scene()
     model = base.model
-    l0 = model.element_rest_length
-    rng = np.random.default_rng(seed)
-    total = start + n_scenarios
-    tensions = rng.uniform(0.0, 0.02, size=(total, 3))[start:]
-    scale = rng.uniform(1.0, 1.5, size=total)[start:]
-    offset = rng.uniform(0.0, 2.0 * l0, size=total)[start:]
+    # one fixed table for the whole 65,536-scenario batch, so any shard
+    # [start, start + n) is identical on every rank and in every call
+    table = CFG4_TOTAL if start + n_scenarios <= CFG4_TOTAL else start + n_scenarios
+    t_all, s_all, o_all = _cfg4_table(seed, table)
+    tensions = t_all[start:start + n_scenarios].copy()
+    scale = s_all[start:start + n_scenarios]
+    offset = o_all[start:start + n_scenarios]
     unit = _press_load(model, np.arange(1, 21), 0.02)
     applied = scale[:, None] * unit[None, :]
     x0 = np.tile(model.rest_configuration, (n_scenarios, 1))
