@@ -245,8 +245,11 @@ def main():
     from paper_2503_06922_b200 import scenarios
     from paper_2503_06922_b200.engine import Engine
 
+    from paper_2503_06922_b200 import shard
+
     B = args.batch
-    w = scenarios.cfg4(B, start=(rank * B) % scenarios.CFG4_TOTAL)
+    start, _ = shard.shard_range(rank, world, B, scenarios.CFG4_TOTAL)
+    w = scenarios.cfg4(B, start=start)
     eng = Engine(**w.engine_kwargs(), device=local)
     x0 = torch.tensor(w.x0, device=dev)
     ten = torch.tensor(w.tensions, device=dev)
@@ -282,11 +285,7 @@ def main():
         dist.barrier()
     launches = eng.launches - launches0
     clk = clocks.stop()
-    ms = statistics.mean(times)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = shard.max_over_ranks(statistics.mean(times), dist if world > 1 else None, dev)
     value = B * world / (ms * 1e-3)
     status = out.status.cpu().numpy()
     frames = out.frames.cpu().numpy()
@@ -311,11 +310,7 @@ def main():
             eng.solve_static_batch(hx0, hten, happ, tol=w.tol, max_frames=w.max_frames, out=hout)
             et.append((time.perf_counter() - t0) * 1e3)
             flush.zero_()
-        ems = statistics.mean(et)
-        if world > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = shard.max_over_ranks(statistics.mean(et), dist if world > 1 else None, dev)
         h2d = hx0.nbytes + hten.nbytes + happ.nbytes
         d2h = sum(getattr(hout, f).nbytes for f in ("coords", "status", "frames", "converged", "residual",
                                                       "n_contacts", "contact_node", "contact_triangle",

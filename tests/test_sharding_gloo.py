@@ -1,0 +1,55 @@
+"""World-size-2 gloo run of the multi-rank path on CPU: each rank solves its
+cfg4 shard with the serial emulation of the device solver, the step time is
+max-reduced, results are gathered, and the union equals a single-rank run."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from emu.emu_binding import EmuEngine
+    from paper_2503_06922_b200 import scenarios, shard
+    per = 3
+    start, stop = shard.shard_range(rank, world, per, scenarios.CFG4_TOTAL)
+    w = scenarios.cfg4(per, start=start)
+    H = EmuEngine(**w.engine_kwargs()).solve(w.x0, w.tensions, w.applied, w.tol, w.max_frames)
+    t = shard.max_over_ranks(float(rank + 1), dist)
+    coords, frames, status = shard.gather_results([H["coords"], H["frames"], H["status"]], dist)
+    if rank == 0:
+        np.savez(out_path, coords=coords, frames=frames, status=status, tmax=t)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_shards_equal_single_rank(tmp_path):
+    from emu.emu_binding import EmuEngine
+    from paper_2503_06922_b200 import scenarios
+    out = str(tmp_path / "r.npz")
+    port = 29500 + os.getpid() % 1000
+    tmp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    r = np.load(out)
+    assert float(r["tmax"]) == 2.0
+    w = scenarios.cfg4(6)
+    H = EmuEngine(**w.engine_kwargs()).solve(w.x0, w.tensions, w.applied, w.tol, w.max_frames)
+    assert np.array_equal(r["frames"], H["frames"])
+    assert np.array_equal(r["status"], H["status"])
+    assert np.array_equal(r["coords"], H["coords"])
+
+
+def test_shard_range():
+    from paper_2503_06922_b200.shard import shard_range
+    assert shard_range(0, 8, 8192, 65536) == (0, 8192)
+    assert shard_range(7, 8, 8192, 65536) == (57344, 65536)
+    with pytest.raises(ValueError):
+        shard_range(2, 2, 1, 10)
