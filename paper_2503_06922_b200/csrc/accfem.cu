@@ -145,7 +145,7 @@ struct accfem_handle {
   DevBuf<double> rest, rest_dir, rest_len, rest_frames, offsets, qa, qb, fixed_inc;
   DevBuf<int> fixed_node, fixed_dof, fixed_row_of_dof, bad;
   DevBuf<double> corners, normals, lo, hi;
-  DevBuf<int> tri_cell_lo, cell_start, cell_tris;
+  DevBuf<int> cell_start, cell_tris;
   DevBuf<double> ws;
   DevBuf<int> counter;
   long ws_stride = 0;
@@ -265,7 +265,6 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
     UP(normals, hm.normals.data(), hm.normals.size());
     UP(lo, hm.lo.data(), hm.lo.size());
     UP(hi, hm.hi.data(), hm.hi.size());
-    UP(tri_cell_lo, hm.tri_cell_lo.data(), hm.tri_cell_lo.size());
     UP(cell_start, hm.cell_start.data(), hm.cell_start.size());
     UP(cell_tris, hm.cell_tris.data(), hm.cell_tris.size());
   }
@@ -278,7 +277,7 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
   MeshDev& G = P.mesh;
   G.T = hm.T;
   G.corners = h->corners.p; G.normals = h->normals.p; G.lo = h->lo.p; G.hi = h->hi.p;
-  G.tri_cell_lo = h->tri_cell_lo.p; G.cell_start = h->cell_start.p; G.cell_tris = h->cell_tris.p;
+  G.cell_start = h->cell_start.p; G.cell_tris = h->cell_tris.p;
   for (int a = 0; a < 3; ++a) {
     G.origin[a] = hm.origin[a];
     G.dims[a] = hm.dims[a];
@@ -335,7 +334,7 @@ extern "C" int accfem_destroy(accfem_handle* h) {
                   &h->h_wy, &h->h_wf, &h->h_rho, &h->o_coords, &h->o_res, &h->o_cd, &h->o_wy, &h->o_wf, &h->o_rho,
                   &h->o_tr})
     b->release();
-  for (auto* b : {&h->fixed_node, &h->fixed_dof, &h->fixed_row_of_dof, &h->bad, &h->tri_cell_lo, &h->cell_start,
+  for (auto* b : {&h->fixed_node, &h->fixed_dof, &h->fixed_row_of_dof, &h->bad, &h->cell_start,
                   &h->cell_tris, &h->counter, &h->o_ints})
     b->release();
   delete h;

@@ -3,11 +3,10 @@
 // the uniform-grid broad-phase structure over the lumen triangles.
 //
 // The grid replaces the reference's median-split AABB tree (mesh.py:199-268):
-// every triangle is listed in each cell its AABB overlaps; a node query walks
-// the cells overlapped by its (slightly enlarged) search box and visits each
-// triangle once, at the first visited cell its AABB covers, then applies the
-// reference's exact AABB-vs-sphere leaf test.  Candidate sets are therefore
-// identical to the tree's leaf test.
+// every cell lists the triangles whose AABB lies within the query radius of
+// the cell; a node query reads its one cell and applies the reference's exact
+// AABB-vs-sphere leaf test to each listed triangle, so candidate sets equal
+// the tree's leaf test.
 #pragma once
 #include <math.h>
 #include <stdint.h>
@@ -23,7 +22,7 @@ namespace accfem_host {
 struct HostMesh {
   int T = 0;
   std::vector<double> corners, normals, lo, hi;
-  std::vector<int> tri_cell_lo, cell_start, cell_tris;
+  std::vector<int> cell_start, cell_tris;
   double origin[3] = {0, 0, 0};
   double inv_h = 1.0;
   int dims[3] = {1, 1, 1};
@@ -71,15 +70,28 @@ inline std::string build_mesh(const accfem_mesh_desc* d, double radius, HostMesh
       bhi[a] = mx > bhi[a] ? mx : bhi[a];
     }
   }
-  // cell size: half the query radius, coarsened until the grid has <= 2^22
-  // cells and the cell lists hold <= 2^23 entries
+  // Uniform grid over the mesh bounds grown by the query radius.  Each cell
+  // lists every triangle whose AABB lies within r of the cell box, so a node
+  // query reads exactly one cell (no de-duplication); a node outside the
+  // grid has no triangle within r.  Cell size starts at r/2 and is coarsened
+  // until the grid has <= 2^22 cells and the lists hold <= 2^24 entries.
+  const double rr = radius * (1.0 + 1e-9) + 1e-12;
+  double glo[3], ghi[3];
+  for (int a = 0; a < 3; ++a) {
+    double pad = rr + 1e-9 * (bhi[a] - blo[a]) + 1e-12;
+    glo[a] = blo[a] - pad;
+    ghi[a] = bhi[a] + pad;
+  }
   double h = radius > 0 ? 0.5 * radius : 1e-3;
   long ncell = 0;
+  auto tri_range = [&](int t, int a, double inv, int dim, int& c0, int& c1) {
+    c0 = grid_cell_host(M.lo[3L * t + a] - rr, glo[a], inv, dim);
+    c1 = grid_cell_host(M.hi[3L * t + a] + rr, glo[a], inv, dim);
+  };
   for (int tries = 0; tries < 200; ++tries) {
     ncell = 1;
     for (int a = 0; a < 3; ++a) {
-      double ext = bhi[a] - blo[a];
-      long da = (long)ceil(ext / h) + 1;
+      long da = (long)ceil((ghi[a] - glo[a]) / h) + 1;
       if (da < 1) da = 1;
       M.dims[a] = (int)da;
       ncell *= da;
@@ -88,35 +100,44 @@ inline std::string build_mesh(const accfem_mesh_desc* d, double radius, HostMesh
     if (ok) {
       double inv = 1.0 / h;
       long entries = 0;
-      for (int t = 0; t < T && entries <= (1L << 23); ++t) {
+      for (int t = 0; t < T && entries <= (1L << 24); ++t) {
         long c = 1;
-        for (int a = 0; a < 3; ++a)
-          c *= grid_cell_host(M.hi[3L * t + a], blo[a], inv, M.dims[a]) -
-               grid_cell_host(M.lo[3L * t + a], blo[a], inv, M.dims[a]) + 1;
+        for (int a = 0; a < 3; ++a) {
+          int c0, c1;
+          tri_range(t, a, inv, M.dims[a], c0, c1);
+          c *= c1 - c0 + 1;
+        }
         entries += c;
       }
-      ok = entries <= (1L << 23);
+      ok = entries <= (1L << 24);
     }
     if (ok) break;
     h *= 1.5;
   }
-  for (int a = 0; a < 3; ++a) M.origin[a] = blo[a];
+  for (int a = 0; a < 3; ++a) M.origin[a] = glo[a];
   M.inv_h = 1.0 / h;
-  M.tri_cell_lo.resize(3L * T);
-  std::vector<int> count(ncell + 1, 0);
-  std::vector<int> chi(3L * T);
-  for (int t = 0; t < T; ++t)
+  // box distance between cell c (padded by 1e-6 h) and the AABB of triangle t
+  auto near = [&](int t, const int* c) {
+    double d2 = 0.0;
     for (int a = 0; a < 3; ++a) {
-      M.tri_cell_lo[3L * t + a] = grid_cell_host(M.lo[3L * t + a], M.origin[a], M.inv_h, M.dims[a]);
-      chi[3L * t + a] = grid_cell_host(M.hi[3L * t + a], M.origin[a], M.inv_h, M.dims[a]);
+      double clo = glo[a] + c[a] * h - 1e-6 * h, chi = glo[a] + (c[a] + 1) * h + 1e-6 * h;
+      double g = 0.0;
+      if (M.lo[3L * t + a] > chi) g = M.lo[3L * t + a] - chi;
+      else if (clo > M.hi[3L * t + a]) g = clo - M.hi[3L * t + a];
+      d2 += g * g;
     }
-  auto cells_of = [&](int t, auto&& fn) {
-    const int* lo = &M.tri_cell_lo[3L * t];
-    const int* hi = &chi[3L * t];
-    for (int z = lo[2]; z <= hi[2]; ++z)
-      for (int y = lo[1]; y <= hi[1]; ++y)
-        for (int x = lo[0]; x <= hi[0]; ++x) fn((z * M.dims[1] + y) * M.dims[0] + x);
+    return d2 <= rr * rr;
   };
+  auto cells_of = [&](int t, auto&& fn) {
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) tri_range(t, a, M.inv_h, M.dims[a], lo[a], hi[a]);
+    int c[3];
+    for (c[2] = lo[2]; c[2] <= hi[2]; ++c[2])
+      for (c[1] = lo[1]; c[1] <= hi[1]; ++c[1])
+        for (c[0] = lo[0]; c[0] <= hi[0]; ++c[0])
+          if (near(t, c)) fn(((long)c[2] * M.dims[1] + c[1]) * M.dims[0] + c[0]);
+  };
+  std::vector<int> count(ncell + 1, 0);
   for (int t = 0; t < T; ++t) cells_of(t, [&](long c) { count[c + 1]++; });
   M.cell_start.assign(ncell + 1, 0);
   for (long c = 0; c < ncell; ++c) M.cell_start[c + 1] = M.cell_start[c] + count[c + 1];

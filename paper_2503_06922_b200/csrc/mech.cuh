@@ -263,12 +263,6 @@ DEV void closest_point(const double* p, const double* a, const double* b, const 
   for (int i = 0; i < 3; ++i) out[i] = xadd(xadd(a[i], xmul(v, ab[i])), xmul(w, ac[i]));
 }
 
-DEV int grid_cell(double x, double o, double inv_h, int dim) {
-  double f = floor((x - o) * inv_h);
-  if (!(f >= 0.0)) return 0;
-  if (f >= (double)(dim - 1)) return dim - 1;
-  return (int)f;
-}
 
 // per-node winner (min signed distance, ties to the lower triangle id),
 // then node-ordered compaction.  Returns the contact count.
@@ -278,56 +272,48 @@ DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws)
   const int N = P.m.N;
   const double margin = P.s.margin, radius = P.s.radius;
   const double r2 = xmul(radius, radius);
-  const double rq = radius * 1.000001 + 1e-12;  // superset box for the grid walk
   PARFOR(k, N) {
     double p[3] = {x[6 * k], x[6 * k + 1], x[6 * k + 2]};
-    int qlo[3], qhi[3];
-    for (int a = 0; a < 3; ++a) {
-      qlo[a] = grid_cell(p[a] - rq, G.origin[a], G.inv_h, G.dims[a]);
-      qhi[a] = grid_cell(p[a] + rq, G.origin[a], G.inv_h, G.dims[a]);
-    }
     int best_t = -1;
     double best_s = 0.0, best_gap = 0.0, best_pp[3] = {0.0, 0.0, 0.0};
-    for (int cz = qlo[2]; cz <= qhi[2]; ++cz)
-      for (int cy = qlo[1]; cy <= qhi[1]; ++cy)
-        for (int cx = qlo[0]; cx <= qhi[0]; ++cx) {
-          int cell = (cz * G.dims[1] + cy) * G.dims[0] + cx;
-          for (int it = G.cell_start[cell]; it < G.cell_start[cell + 1]; ++it) {
-            int t = G.cell_tris[it];
-            const int* tc = G.tri_cell_lo + 3 * t;
-            // visit each triangle once: at the first query cell its AABB covers
-            int ox = tc[0] > qlo[0] ? tc[0] : qlo[0];
-            int oy = tc[1] > qlo[1] ? tc[1] : qlo[1];
-            int oz = tc[2] > qlo[2] ? tc[2] : qlo[2];
-            if (ox != cx || oy != cy || oz != cz) continue;
-            // exact reference AABB-vs-sphere leaf test (mesh.py:259-262)
-            double gg[3];
-            for (int a = 0; a < 3; ++a) {
-              double lo = G.lo[3 * t + a], hi = G.hi[3 * t + a];
-              double u = xsub(lo, p[a]), v = xsub(p[a], hi);
-              v = v > 0.0 ? v : 0.0;
-              gg[a] = u > v ? u : v;
-            }
-            if (!(edot3(gg, gg) <= r2)) continue;
-            const double* cor = G.corners + 9 * t;
-            double cl[3], off[3];
-            closest_point(p, cor, cor + 3, cor + 6, cl);
-            for (int a = 0; a < 3; ++a) off[a] = xsub(p[a], cl[a]);
-            double eu = enorm3(off);
-            double pg = edot3(G.normals + 3 * t, off);
-            double sg = pg >= 0.0 ? eu : -eu;
-            bool aligned = fabs(pg) >= xsub(xmul(0.9, eu), 1e-12);
-            if (!(sg <= margin && eu <= radius && aligned)) continue;
-            if (best_t < 0 || sg < best_s || (sg == best_s && t < best_t)) {
-              best_t = t;
-              best_s = sg;
-              best_gap = pg;
-              best_pp[0] = cl[0];
-              best_pp[1] = cl[1];
-              best_pp[2] = cl[2];
-            }
-          }
-        }
+    int c[3];
+    bool inside = true;
+    for (int a = 0; a < 3; ++a) {
+      double f = floor((p[a] - G.origin[a]) * G.inv_h);
+      inside = inside && (f >= 0.0) && (f < (double)G.dims[a]);
+      c[a] = inside ? (int)f : 0;
+    }
+    const int cell = inside ? (c[2] * G.dims[1] + c[1]) * G.dims[0] + c[0] : 0;
+    const int it0 = inside ? G.cell_start[cell] : 0, it1 = inside ? G.cell_start[cell + 1] : 0;
+    for (int it = it0; it < it1; ++it) {
+      const int t = G.cell_tris[it];
+      // exact reference AABB-vs-sphere leaf test (mesh.py:259-262)
+      double gg[3];
+      for (int a = 0; a < 3; ++a) {
+        double lo = G.lo[3 * t + a], hi = G.hi[3 * t + a];
+        double u = xsub(lo, p[a]), v = xsub(p[a], hi);
+        v = v > 0.0 ? v : 0.0;
+        gg[a] = u > v ? u : v;
+      }
+      if (!(edot3(gg, gg) <= r2)) continue;
+      const double* cor = G.corners + 9 * t;
+      double cl[3], off[3];
+      closest_point(p, cor, cor + 3, cor + 6, cl);
+      for (int a = 0; a < 3; ++a) off[a] = xsub(p[a], cl[a]);
+      double eu = enorm3(off);
+      double pg = edot3(G.normals + 3 * t, off);
+      double sg = pg >= 0.0 ? eu : -eu;
+      bool aligned = fabs(pg) >= xsub(xmul(0.9, eu), 1e-12);
+      if (!(sg <= margin && eu <= radius && aligned)) continue;
+      if (best_t < 0 || sg < best_s || (sg == best_s && t < best_t)) {
+        best_t = t;
+        best_s = sg;
+        best_gap = pg;
+        best_pp[0] = cl[0];
+        best_pp[1] = cl[1];
+        best_pp[2] = cl[2];
+      }
+    }
     ws.ctri[k] = best_t;
     ws.cgap[k] = best_gap;
     ws.cpp[3 * k] = best_pp[0];

@@ -51,9 +51,8 @@ struct MeshDev {
   const double* normals;      // T x 3
   const double* lo;           // T x 3 triangle AABB
   const double* hi;           // T x 3
-  const int* tri_cell_lo;     // T x 3 clamped grid cell of the AABB lo corner
   const int* cell_start;      // ncell + 1
-  const int* cell_tris;       // CSR payload, ascending triangle id per cell
+  const int* cell_tris;       // CSR: triangles whose AABB is within the query radius of the cell
   double origin[3];
   double inv_h;
   int dims[3];

@@ -80,7 +80,7 @@ extern "C" EmuHandle* emu_create(const accfem_model_desc* md, const accfem_mesh_
   if (G.T) {
     G.corners = h->mesh.corners.data(); G.normals = h->mesh.normals.data();
     G.lo = h->mesh.lo.data(); G.hi = h->mesh.hi.data();
-    G.tri_cell_lo = h->mesh.tri_cell_lo.data(); G.cell_start = h->mesh.cell_start.data();
+    G.cell_start = h->mesh.cell_start.data();
     G.cell_tris = h->mesh.cell_tris.data();
     for (int a = 0; a < 3; ++a) { G.origin[a] = h->mesh.origin[a]; G.dims[a] = h->mesh.dims[a]; }
     G.inv_h = h->mesh.inv_h;
