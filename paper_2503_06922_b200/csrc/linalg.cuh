@@ -607,26 +607,42 @@ DEV void twisted_solve_multi(const TeamWarp& team, int N, const double* __restri
 }
 #endif
 
-// y = M x for a symmetric block-tridiagonal (D, U) matrix; y must not alias x
+// y = M x for a symmetric block-tridiagonal (D, U) matrix (full 6x6 diagonal
+// blocks); y must not alias x.  Four rows per lane per pass keep four
+// independent load streams in flight (the blocks live in L2).
+DEV double bt_row(int N, const double* D, const double* U, const double* x, int j) {
+  const int k = j / 6, r = j - 6 * k;
+  const double* dr = D + 36 * k + 6 * r;
+  const double* xk = x + 6 * k;
+  double acc = dr[0] * xk[0] + dr[1] * xk[1] + dr[2] * xk[2] + dr[3] * xk[3] + dr[4] * xk[4] + dr[5] * xk[5];
+  if (k + 1 < N) {
+    const double* ur = U + 36 * k + 6 * r;
+    const double* xn = x + 6 * (k + 1);
+    acc += ur[0] * xn[0] + ur[1] * xn[1] + ur[2] * xn[2] + ur[3] * xn[3] + ur[4] * xn[4] + ur[5] * xn[5];
+  }
+  if (k > 0) {
+    const double* up = U + 36 * (k - 1) + r;
+    const double* xp = x + 6 * (k - 1);
+    acc += up[0] * xp[0] + up[6] * xp[1] + up[12] * xp[2] + up[18] * xp[3] + up[24] * xp[4] + up[30] * xp[5];
+  }
+  return acc;
+}
+
 template <class Team>
 DEV void block_matvec(const Team& team, int N, const double* D, const double* U, const double* x, double* y) {
-  PARFOR(j, 6 * N) {
-    int k = j / 6, r = j % 6;
-    const double* dr = D + 36 * k + 6 * r;
-    const double* xk = x + 6 * k;
-    double acc = 0.0;
-    for (int c = 0; c < 6; ++c) acc += dr[c] * xk[c];
-    if (k + 1 < N) {
-      const double* ur = U + 36 * k + 6 * r;
-      const double* xn = x + 6 * (k + 1);
-      for (int c = 0; c < 6; ++c) acc += ur[c] * xn[c];
-    }
-    if (k > 0) {
-      const double* up = U + 36 * (k - 1);
-      const double* xp = x + 6 * (k - 1);
-      for (int c = 0; c < 6; ++c) acc += up[6 * c + r] * xp[c];
-    }
-    y[j] = acc;
+  const int n = 6 * N;
+  const int stride = team.size();
+  for (int j0 = team.rank(); j0 < n; j0 += 4 * stride) {
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    const int j1 = j0 + stride, j2 = j0 + 2 * stride, j3 = j0 + 3 * stride;
+    a0 = bt_row(N, D, U, x, j0);
+    if (j1 < n) a1 = bt_row(N, D, U, x, j1);
+    if (j2 < n) a2 = bt_row(N, D, U, x, j2);
+    if (j3 < n) a3 = bt_row(N, D, U, x, j3);
+    y[j0] = a0;
+    if (j1 < n) y[j1] = a1;
+    if (j2 < n) y[j2] = a2;
+    if (j3 < n) y[j3] = a3;
   }
   team.sync();
 }

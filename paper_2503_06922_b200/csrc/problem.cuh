@@ -80,7 +80,7 @@ struct Ws {
   // scaled system; HD/HU hold H_s, then M, then its twisted factor in place
   double *HD, *HU, *gs, *d, *colh, *xs, *xt, *rhs, *w, *v, *tmp;
   // solution / polish
-  double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr;
+  double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr, *W, *Sf, *Cv;
   int *act, *alist;
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
   bool sh;                   // hot arrays live in shared memory
@@ -120,6 +120,9 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   w.d = take(n); w.colh = take(n); w.w = take(n); w.v = take(n);
   w.dx = take(n); w.dxp = take(n); w.yp = take(m); w.S = take(cp * cp); w.Sy = take(3 * cp);
   w.Wc = take(2 * kMultiRhs * n);
+  w.W = take(cp * n);      // polish: P^{-1} C~_c for every contact c
+  w.Sf = take(cp * cp);    // polish: C P^{-1} C~^T over all contacts
+  w.Cv = take(cp);
   w.wfix = take(n);
   w.scr = take(160);
   double* ib = take((5L * N + m + 8) / 2 + 1);

@@ -144,9 +144,13 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   double c = 1.0;
   double* dd = ws.tmp;  // hot scratch: unused until the ADMM loop
   double* ee = ws.tr;
+  double gam_prev = 1.0;
+  double* colg = ws.colh;  // column maxima of H from the previous sweep's cost pass
   for (int sweep = 0; sweep < P.s.scaling_iterations; ++sweep) {
     PARFOR(j, n) {
-      double mx = hcol_max(ws.HD, ws.HU, N, j);
+      // H part: max |gam h| = gam * max |h| exactly (rounding is monotone), so
+      // sweeps after the first reuse the previous cost-normalisation pass
+      double mx = sweep == 0 ? hcol_max(ws.HD, ws.HU, N, j) : gam_prev * colg[j];
       int fr = P.m.fixed_row_of_dof[j];
       if (fr >= 0) mx = fmax(mx, fabs(ws.as[3 * fr]));
       int cc = j % 6;
@@ -188,12 +192,15 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
     // cost normalisation: column maxima of the scaled H only
     double csum = 0.0, gmax = 0.0;
     PARFOR(j, n) {
-      csum += hcol_max(ws.HD, ws.HU, N, j);
+      const double cm = hcol_max(ws.HD, ws.HU, N, j);
+      colg[j] = cm;
+      csum += cm;
       gmax = fmax(gmax, fabs(ws.gs[j]));
     }
     csum = team.sum(csum);
     gmax = team.max(gmax);
     double gam = 1.0 / fmax(fmax(csum / n, gmax), 1e-12);
+    gam_prev = gam;
     PARFOR(i, 21 * N) {
       int k = i / 21;
       ws.HD[kDiag * k + (i - 21 * k)] *= gam;
@@ -416,48 +423,32 @@ DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
   team.sync();
 }
 
-// one regularised solve of [[H+dI, C^T], [C, -dI]] [x; y] = [f; h] with the
-// selector DOFs eliminated (x_F = f_F).  f is a full-length vector; h is
-// indexed by active-contact slot.  Uses the factored S.  x -> xo, y -> yo.
+// active-set polish (solver.py:449-528).  On entry ws.dx / ws.yfull hold the
+// ADMM result (yfull unclipped); on acceptance they are replaced.
+//
+// Every round solves the regularised reduced KKT [[H+dI, C^T], [C, -dI]] of
+// the active rows with the selector DOFs eliminated exactly, through a dense
+// Schur complement over the active contacts.  P = H + dI (reduced) is factored
+// once; W_c = P^{-1} C~_c for ALL contacts, S = C W and v = P^{-1} f are
+// formed once per polish, so a round costs one block solve (the refinement
+// round of _solve_active_subset) plus dense work on the active submatrix.
 template <class Team>
-DEV void schur_solve(const Team& team, const Problem& P, Ws& ws, int na, const double* f, const double* h,
-                     double* xo, double* yo) {
-  const int N = P.m.N, n = 6 * N;
-  twisted_solve(team, N, ws.HD, ws.HU, f, ws.tmp, ws.v, 1, 0, ws.sh);
-  team.sync();
-  PARFOR(q, na) {
-    int c = ws.alist[q];
-    const double* nr = ws.cnrm + 3 * c;
-    const double* vv = ws.v + 6 * ws.cnode[c];
-    yo[q] = (nr[0] * vv[0] + nr[1] * vv[1] + nr[2] * vv[2]) - h[q];
+DEV void dense_combine(const Team& team, int n, int na, const int* alist, const double* W, const double* y,
+                       const double* base, double* out) {
+  PARFOR(j, n) {
+    double acc = base[j];
+    for (int q = 0; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
+    out[j] = acc;
   }
-  team.sync();
-  if (na > 0) dense_solve(team, na, ws.S, yo);
-  // x = v - P^{-1} C~^T y
-  PARFOR(j, n) ws.rhs[j] = 0.0;
-  team.sync();
-  PARFOR(q, na) {
-    int c = ws.alist[q];
-    int nd = ws.cnode[c];
-    for (int a = 0; a < 3; ++a) {
-      int j = 6 * nd + a;
-      if (P.m.fixed_row_of_dof[j] < 0) ws.rhs[j] += ws.cnrm[3 * c + a] * yo[q];
-    }
-  }
-  team.sync();
-  twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.w, 1, 0, ws.sh);
-  team.sync();
-  PARFOR(j, n) xo[j] = ws.v[j] - ws.w[j];
   team.sync();
 }
 
-// active-set polish (solver.py:449-528).  On entry ws.dx / ws.yfull hold the
-// ADMM result (yfull unclipped); on acceptance they are replaced.
 template <class Team>
 DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
   const int N = P.m.N, n = 6 * N, nf = F.nf, nc = F.nc;
   const double tol_act = fmax(10.0 * P.s.eps_abs, 1e-12);
   const double delta = 1e-9;
+  if (nc > cmax) return ST_CAPACITY;
   PARFOR(c, nc) {
     int r = nf + c;
     double yc = fmax(ws.yfull[r], 0.0);
@@ -466,9 +457,40 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
   }
   team.sync();
   if (reduced_factor(team, P, delta, ws) >= 0) return ST_OK;  // splu failure -> no polish
+  // W_c = P^{-1} C~_c, 16 contacts per warp pass (C~: contact row with selector DOFs zeroed)
+  for (int c0 = 0; c0 < nc; c0 += kMultiRhs) {
+    const int nb = nc - c0 < kMultiRhs ? nc - c0 : kMultiRhs;
+    double* Wb = ws.W + (long)c0 * n;
+    PARFOR(t, nb * n) Wb[t] = 0.0;
+    team.sync();
+    PARFOR(b, nb) {
+      const int c = c0 + b, nd = ws.cnode[c];
+      for (int a = 0; a < 3; ++a) {
+        const int j = 6 * nd + a;
+        if (P.m.fixed_row_of_dof[j] < 0) Wb[(long)b * n + j] = ws.cnrm[3 * c + a];
+      }
+    }
+    team.sync();
+    twisted_solve_multi(team, N, ws.HD, ws.HU, Wb, ws.Wc, Wb, nb, n);
+    team.sync();
+  }
+  PARFOR(t, nc * nc) {
+    const int p = t / nc, q = t - p * nc;
+    const double* nr = ws.cnrm + 3 * p;
+    const double* wq = ws.W + (long)q * n + 6 * ws.cnode[p];
+    ws.Sf[t] = nr[0] * wq[0] + nr[1] * wq[1] + nr[2] * wq[2];
+  }
+  // v = P^{-1} f with f the eliminated right-hand side; Cv_c = C_c v
+  eliminated_rhs(team, P, F, ws, ws.xt);
+  twisted_solve(team, N, ws.HD, ws.HU, ws.xt, ws.tmp, ws.v, 1, 0, ws.sh);
+  team.sync();
+  PARFOR(c, nc) ws.Cv[c] = row_dot(P, F, ws, nf + c, ws.v);
+  team.sync();
   bool found = false;
   double* dxp = ws.dxp;
   double* yp = ws.yp;
+  double* yact = ws.Sy + cmax;      // na entries
+  double* dyq = ws.Sy + 2 * cmax;   // na entries
   for (int round = 0; round < 6; ++round) {
     // active contact list in row order
     int na = 0;
@@ -477,79 +499,51 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
       bool a = c < nc && ws.act[c];
       int tot = 0;
       int pos = team.ballot_prefix(a, &tot);
-      if (team.size() == 1) {
-        if (a) ws.alist[na] = c;
-      } else if (a) {
-        ws.alist[na + pos] = c;
-      }
+      if (a) ws.alist[na + pos] = c;
       na += tot;
     }
     team.sync();
     PARFOR(q, na) ws.alist[N + ws.alist[q]] = q;
     team.sync();
     if (nf + na == 0) break;
-    if (na > cmax) return ST_CAPACITY;
-    // S = C~ P^{-1} C~^T + delta I, columns in batches of kMultiRhs
-    for (int q0 = 0; q0 < na; q0 += kMultiRhs) {
-      int nb = na - q0 < kMultiRhs ? na - q0 : kMultiRhs;
-      PARFOR(t, nb * n) ws.Wc[t] = 0.0;
-      team.sync();
-      PARFOR(b, nb) {
-        int c = ws.alist[q0 + b];
-        int nd = ws.cnode[c];
-        for (int a = 0; a < 3; ++a) {
-          int j = 6 * nd + a;
-          if (P.m.fixed_row_of_dof[j] < 0) ws.Wc[b * n + j] = ws.cnrm[3 * c + a];
-        }
-      }
-      team.sync();
-      twisted_solve_multi(team, N, ws.HD, ws.HU, ws.Wc, ws.Wc + kMultiRhs * n, ws.Wc, nb, n);
-      team.sync();
-      PARFOR(t, na * nb) {
-        int p = t / nb, b = t % nb;
-        int c = ws.alist[p];
-        const double* nr = ws.cnrm + 3 * c;
-        const double* ww = ws.Wc + b * n + 6 * ws.cnode[c];
-        double v = nr[0] * ww[0] + nr[1] * ww[1] + nr[2] * ww[2];
-        if (p == q0 + b) v += delta;
-        ws.S[p * na + q0 + b] = v;
-      }
-      team.sync();
-    }
-    // symmetrise (the two triangles agree to rounding) and factor
+    // S_a = S[act, act] + delta I, factored
     PARFOR(t, na * na) {
-      int p = t / na, q = t % na;
-      if (q > p) ws.S[q * na + p] = ws.S[p * na + q];
+      const int p = t / na, q = t - p * na;
+      const int cp = ws.alist[p], cq = ws.alist[q];
+      // the two triangles of C P^{-1} C~^T agree to rounding; use the lower one
+      double v = cp >= cq ? ws.Sf[cp * nc + cq] : ws.Sf[cq * nc + cp];
+      ws.S[t] = v + (p == q ? delta : 0.0);
     }
     team.sync();
     if (na > 0 && !dense_chol(team, na, ws.S)) return ST_OK;
-    // first solve: f = eliminated rhs, h = b_C
-    eliminated_rhs(team, P, F, ws, ws.xt);
-    PARFOR(q, na) ws.Sy[q] = ws.up[nf + ws.alist[q]];
+    // y = S_a^{-1} (C v - b_C);  dx = v - W_act y
+    PARFOR(q, na) yact[q] = ws.Cv[ws.alist[q]] - ws.up[nf + ws.alist[q]];
     team.sync();
-    double* yact = ws.Sy + cmax;  // na entries
-    schur_solve(team, P, ws, na, ws.xt, ws.Sy, dxp, yact);
-    // one refinement round against the exact KKT
-    PARFOR(j, n) ws.tmp[j] = 0.0;
-    team.sync();
+    if (na > 0) dense_solve(team, na, ws.S, yact);
+    dense_combine(team, n, na, ws.alist, ws.W, yact, ws.v, dxp);
+    // one refinement round against the exact KKT (solver.py:514-522)
     block_matvec(team, N, ws.KD, ws.KU, dxp, ws.xt);
     PARFOR(j, n) {
-      bool fx = P.m.fixed_row_of_dof[j] >= 0;
+      const bool fx = P.m.fixed_row_of_dof[j] >= 0;
       double ct = 0.0;
-      int k = j / 6, a = j % 6;
+      const int k = j / 6, a = j % 6;
       if (a < 3) {
-        int c = ws.crow_of_node[k];
+        const int c = ws.crow_of_node[k];
         if (c >= 0 && ws.act[c]) ct = ws.cnrm[3 * c + a] * yact[ws.alist[N + c]];
       }
       ws.xt[j] = fx ? 0.0 : -ws.g[j] - ws.xt[j] - ct;
     }
+    team.sync();
+    twisted_solve(team, N, ws.HD, ws.HU, ws.xt, ws.tmp, ws.w, 1, 0, ws.sh);
+    team.sync();
     PARFOR(q, na) {
-      int c = ws.alist[q];
-      ws.Sy[q] = ws.up[nf + c] - row_dot(P, F, ws, nf + c, dxp);
+      const int c = ws.alist[q];
+      const double r2 = ws.up[nf + c] - row_dot(P, F, ws, nf + c, dxp);
+      dyq[q] = row_dot(P, F, ws, nf + c, ws.w) - r2;
     }
     team.sync();
-    double* dyq = ws.Sy + 2 * cmax;
-    schur_solve(team, P, ws, na, ws.xt, ws.Sy, ws.colh, dyq);
+    if (na > 0) dense_solve(team, na, ws.S, dyq);
+    dense_combine(team, n, na, ws.alist, ws.W, dyq, ws.w, ws.colh);
     PARFOR(j, n) dxp[j] += ws.colh[j];
     PARFOR(q, na) yact[q] += dyq[q];
     team.sync();
