@@ -452,24 +452,16 @@ DEV void twisted_solve_impl(const TeamWarp& team, int N, const double* __restric
   }
   __syncwarp();  // sweep-1 values visible; rhs fully consumed (out may alias rhs)
   // ---- z_i = Dinv_i v_i for every block but k; lane handles (block, row) pairs
-  {
-    int i = lane / 6, rr = lane % 6;  // q = 6 i + rr, stepping by 32 = 5 blocks + 2 rows
-    for (int q = lane; q < 6 * N; q += 32) {
-      if (i != k) {
-        const double* Di = D + kDiag * i;
-        const double* vi = tmp + 6 * i;
-        const double z = (Di[sidx(rr, 0)] * vi[0] + Di[sidx(rr, 2)] * vi[2] + Di[sidx(rr, 4)] * vi[4]) +
-                         (Di[sidx(rr, 1)] * vi[1] + Di[sidx(rr, 3)] * vi[3] + Di[sidx(rr, 5)] * vi[5]);
-        out[q] = z;  // out != tmp: z parked in out, consumed below before x_i overwrites it
-      }
-      rr += 2;
-      i += 5;
-      if (rr >= 6) {
-        rr -= 6;
-        i += 1;
-      }
+  parfor4(team, 6 * N, [&](int q) {
+    const int i = q / 6, rr = q - 6 * i;
+    if (i != k) {
+      const double* Di = D + kDiag * i;
+      const double* vi = tmp + 6 * i;
+      const double z = (Di[sidx(rr, 0)] * vi[0] + Di[sidx(rr, 2)] * vi[2] + Di[sidx(rr, 4)] * vi[4]) +
+                       (Di[sidx(rr, 1)] * vi[1] + Di[sidx(rr, 3)] * vi[3] + Di[sidx(rr, 5)] * vi[5]);
+      out[q] = z;  // out != tmp: z parked in out, consumed below before x_i overwrites it
     }
-  }
+  });
   __syncwarp();
   if (sub == 0) out[6 * k + r] = xk;
   // ---- sweep 2: top x_i = z_i - X_{i+1}^T x_{i+1}, i = k-1-t; bottom x_i = z_i - Y_{i-1}^T x_{i-1}, i = k+1+t

@@ -124,11 +124,11 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
     sym_rc(p, r, c);
     ws.HD[kDiag * k + p] = ws.KD[36 * k + 6 * r + c];
   }
-  PARFOR(i, 36 * E) ws.HU[i] = ws.KU[i];
-  PARFOR(j, n) {
+  parfor4(team, 36 * E, [&](int i) { ws.HU[i] = ws.KU[i]; });
+  parfor4(team, n, [&](int j) {
     ws.gs[j] = ws.g[j];
     ws.d[j] = 1.0;
-  }
+  });
   PARFOR(r, m) {
     ws.e[r] = 1.0;
     if (r < nf) {
@@ -166,15 +166,15 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
       ee[r] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
     }
     team.sync();
-    PARFOR(i, 21 * N) {
+    parfor4(team, 21 * N, [&](int i) {
       int k = i / 21, p = i - 21 * k, r, cc;
       sym_rc(p, r, cc);
       ws.HD[kDiag * k + p] *= dd[6 * k + r] * dd[6 * k + cc];
-    }
-    PARFOR(i, 36 * E) {
+    });
+    parfor4(team, 36 * E, [&](int i) {
       int k = i / 36, t = i - 36 * k, r = t / 6, cc = t - 6 * r;
       ws.HU[i] *= dd[6 * k + r] * dd[6 * (k + 1) + cc];
-    }
+    });
     PARFOR(r, m) {
       if (r < nf) {
         ws.as[3 * r] *= ee[r] * dd[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
@@ -184,10 +184,10 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
       }
       ws.e[r] *= ee[r];
     }
-    PARFOR(j, n) {
+    parfor4(team, n, [&](int j) {
       ws.gs[j] *= dd[j];
       ws.d[j] *= dd[j];
-    }
+    });
     team.sync();
     // cost normalisation: column maxima of the scaled H only
     double csum = 0.0, gmax = 0.0;
@@ -201,12 +201,12 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
     gmax = team.max(gmax);
     double gam = 1.0 / fmax(fmax(csum / n, gmax), 1e-12);
     gam_prev = gam;
-    PARFOR(i, 21 * N) {
+    parfor4(team, 21 * N, [&](int i) {
       int k = i / 21;
       ws.HD[kDiag * k + (i - 21 * k)] *= gam;
-    }
-    PARFOR(i, 36 * E) ws.HU[i] *= gam;
-    PARFOR(j, n) ws.gs[j] *= gam;
+    });
+    parfor4(team, 36 * E, [&](int i) { ws.HU[i] *= gam; });
+    parfor4(team, n, [&](int j) { ws.gs[j] *= gam; });
     c *= gam;
     team.sync();
   }
@@ -225,7 +225,7 @@ DEV Residuals unscaled_residuals(const Team& team, const Problem& P, const Frame
                                  double gnorm) {
   const int N = P.m.N, n = 6 * N;
   double* xu = ws.tmp;
-  PARFOR(j, n) xu[j] = ws.d[j] * ws.xs[j];
+  parfor4(team, n, [&](int j) { xu[j] = ws.d[j] * ws.xs[j]; });
   team.sync();
   double pri = 0.0, ps = 0.0;
   PARFOR(r, F.m) {
@@ -435,11 +435,11 @@ DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
 template <class Team>
 DEV void dense_combine(const Team& team, int n, int na, const int* alist, const double* W, const double* y,
                        const double* base, double* out) {
-  PARFOR(j, n) {
+  parfor4(team, n, [&](int j) {
     double acc = base[j];
     for (int q = 0; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
     out[j] = acc;
-  }
+  });
   team.sync();
 }
 
@@ -666,15 +666,17 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   }
   team.sync();
   const double al = S.alpha, sg = S.sigma;
+  parfor4(team, n, [&](int j) { ws.rhs[j] = sg * ws.xs[j] - ws.gs[j]; });
+  team.sync();
   double rho_est = rho_bar;
   int k = 0;
   bool infeas = false;
   PROF_T0(t_iter);
   for (k = 1; k <= S.max_iterations; ++k) {
-    // rhs = sigma x - g_s + A_s^T (rho o (z - y / rho)); selector rows touch
-    // distinct DOFs, contact rows distinct nodes: two conflict-free passes
-    PARFOR(j, n) ws.rhs[j] = sg * ws.xs[j] - ws.gs[j];
-    team.sync();
+    // rhs = sigma x - g_s + A_s^T (rho o (z - y / rho)); the first term is
+    // written by the previous iteration's x update (or before the loop);
+    // selector rows touch distinct DOFs, contact rows distinct nodes: two
+    // conflict-free passes
     PARFOR(r, nf) {
       double t = ws.rho[r] * (ws.z[r] - ws.y[r] / ws.rho[r]);
       ws.rhs[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]] += ws.as[3 * r] * t;
@@ -708,7 +710,12 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
       ws.y[r] = y + rh * (zr - zn);
       ws.z[r] = zn;
     }
-    PARFOR(j, n) ws.xs[j] = al * ws.xt[j] + (1.0 - al) * ws.xs[j];
+    // x update fused with the next iteration's rhs = sigma x - g_s (xt aliases rhs)
+    parfor4(team, n, [&](int j) {
+      const double xn = al * ws.xt[j] + (1.0 - al) * ws.xs[j];
+      ws.xs[j] = xn;
+      ws.rhs[j] = sg * xn - ws.gs[j];
+    });
     team.sync();
     if (k <= 8 || k % S.check_interval == 0 || k == S.max_iterations) {
       PROF_T0(t_chk);

@@ -24,6 +24,21 @@
 
 #define PARFOR(i, n) for (int i = team.rank(); i < (n); i += team.size())
 
+// strided loop with four independent bodies per pass, so the loads of four
+// elements are in flight together (plain PARFOR bodies run one at a time)
+template <class Team, class F>
+DEV void parfor4(const Team& team, int n, F&& f) {
+  const int s = team.size();
+  int j = team.rank();
+  for (; j + 3 * s < n; j += 4 * s) {
+    f(j);
+    f(j + s);
+    f(j + 2 * s);
+    f(j + 3 * s);
+  }
+  for (; j < n; j += s) f(j);
+}
+
 // phase timers (development builds with -DACCFEM_PROFILE only)
 #if defined(__CUDA_ARCH__) && defined(ACCFEM_PROFILE)
 #define PROF_T0(v) long long v = clock64()
