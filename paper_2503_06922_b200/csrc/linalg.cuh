@@ -131,7 +131,7 @@ DEV void st6(double* p, const double* a) {
 
 // In-place twisted factorisation (D packed, kDiag per block; U full 6x6).
 // Returns the block of a failed pivot, or -1.
-DEVNI bool schur_block(bool top, const double* Ap, const double* C, const double* P, double* Xout, double* Dout) {
+DEV bool schur_block(bool top, const double* Ap, const double* C, const double* P, double* Xout, double* Dout) {
   double X[36], S[36];
 #pragma unroll
   for (int r = 0; r < 6; ++r)
@@ -293,7 +293,7 @@ DEV void twisted_solve_multi(const TeamSerial& t, int N, const double* D, const 
 #if defined(__CUDACC__)
 // Warp factorisation: lane 0 runs the top recursion, lane 1 the bottom one,
 // each 6x6 step entirely in registers; they meet at the middle block.
-DEVNI int twisted_factor_impl(const TeamWarp& team, int N, double* D, double* U, double* scratch) {
+DEV int twisted_factor_impl(const TeamWarp& team, int N, double* D, double* U, double* scratch) {
   const int lane = team.lane;
   const int k = twist_split(N);
   int fail = 1 << 30;
