@@ -52,7 +52,7 @@ constexpr int kTraceStats = 12;  // dx_norm, act_scale, max_pen, compl_worst, re
 
 // one frame.  x (6N) is advanced in place.  Returns a status.
 template <class Team>
-DEVNI int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s, double* x, double insertion,
+DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s, double* x, double insertion,
                    const double* tensions, const double* applied, Ws& ws, double& rho, int& has_wfix,
                    bool& pending, double& resid_prev, FrameStats& st, Frame& F) {
   const ModelDev& M = P.m;

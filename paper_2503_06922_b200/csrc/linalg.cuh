@@ -501,7 +501,7 @@ DEV void twisted_solve(const TeamWarp& team, int N, const double* D, const doubl
 // Many right-hand sides (g < 16): lanes 2g / 2g+1 sweep the top / bottom half
 // of RHS g with the full 6x6 mat-vec in registers; the z_i = Dinv_i v_i
 // products run across all lanes between the sweeps.  out may alias rhs.
-DEVNI void twisted_solve_multi(const TeamWarp& team, int N, const double* __restrict__ D,
+DEV void twisted_solve_multi(const TeamWarp& team, int N, const double* __restrict__ D,
                              const double* __restrict__ U, const double* rhs, double* tmp, double* out, int nrhs,
                              long stride) {
   const int lane = team.lane;

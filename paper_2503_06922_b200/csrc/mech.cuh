@@ -29,7 +29,7 @@ DEV void element_frame(const double* ch, double len, const double* Ra, const dou
 // directors, chord lengths, rest element frames E0 (identity offsets),
 // offsets mean0^T E0 and the fused rest products T0^T E0 of both ends.
 template <class Team>
-DEVNI void model_setup(const Team& team, int N, const double* rest, double* rest_dir, double* rest_len,
+DEV void model_setup(const Team& team, int N, const double* rest, double* rest_dir, double* rest_len,
                      double* rest_frames, double* offsets, double* qa, double* qb, int* bad) {
   PARFOR(k, N) rot_exp(rest + 6 * k + 3, rest_dir + 9 * k);
   team.sync();
@@ -72,7 +72,7 @@ DEV void directors_pass(const Team& team, const Problem& P, const double* x, Ws&
 // tangent.  Returns 0, or the 1-based index of the first degenerate element
 // (beam.py:262-264).
 template <class Team>
-DEVNI int element_pass(const Team& team, const Problem& P, const double* x, Ws& ws, bool tangent) {
+DEV int element_pass(const Team& team, const Problem& P, const double* x, Ws& ws, bool tangent) {
   const ModelDev& M = P.m;
   const int N = M.N, E = N - 1;
   directors_pass(team, P, x, ws);
@@ -180,7 +180,7 @@ DEVNI int element_pass(const Team& team, const Problem& P, const double* x, Ws& 
 
 // F_a = cable wrench at the last node + applied + uniform  (engine.py:108-121)
 template <class Team>
-DEVNI void external_force(const Team& team, const Problem& P, const double* tensions, const double* applied,
+DEV void external_force(const Team& team, const Problem& P, const double* tensions, const double* applied,
                         Ws& ws) {
   const ModelDev& M = P.m;
   const int n = 6 * M.N;
@@ -267,7 +267,7 @@ DEV void closest_point(const double* p, const double* a, const double* b, const 
 // per-node winner (min signed distance, ties to the lower triangle id),
 // then node-ordered compaction.  Returns the contact count.
 template <class Team>
-DEVNI int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws) {
+DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws) {
   const MeshDev& G = P.mesh;
   const int N = P.m.N;
   const double margin = P.s.margin, radius = P.s.radius;

@@ -116,7 +116,7 @@ DEV double hcol_max(const double* HD, const double* HU, int N, int j) {
 }
 
 template <class Team>
-DEVNI double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
+DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   const int N = P.m.N, n = 6 * N, E = N - 1;
   const int nf = F.nf, m = F.m;
   PARFOR(i, 21 * N) {
@@ -221,7 +221,7 @@ struct Residuals {
 };
 
 template <class Team>
-DEVNI Residuals unscaled_residuals(const Team& team, const Problem& P, const Frame& F, Ws& ws, double c,
+DEV Residuals unscaled_residuals(const Team& team, const Problem& P, const Frame& F, Ws& ws, double c,
                                  double gnorm) {
   const int N = P.m.N, n = 6 * N;
   double* xu = ws.tmp;
@@ -253,7 +253,7 @@ DEVNI Residuals unscaled_residuals(const Team& team, const Problem& P, const Fra
 
 // OSQP-style primal infeasibility test on the dual increment (solver.py:424-446)
 template <class Team>
-DEVNI bool infeasible(const Team& team, const Problem& P, const Frame& F, Ws& ws, double c) {
+DEV bool infeasible(const Team& team, const Problem& P, const Frame& F, Ws& ws, double c) {
   const int n = 6 * P.m.N;
   double nd = 0.0;
   PARFOR(r, F.m) {
@@ -287,7 +287,7 @@ DEVNI bool infeasible(const Team& team, const Problem& P, const Frame& F, Ws& ws
 // in HD/HU
 // ---------------------------------------------------------------------------
 template <class Team>
-DEVNI int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws) {
+DEV int reduced_factor(const Team& team, const Problem& P, double delta, Ws& ws) {
   const int N = P.m.N, E = N - 1;
   const int* frd = P.m.fixed_row_of_dof;
   PARFOR(i, 21 * N) {
@@ -348,7 +348,7 @@ DEV void selector_multipliers(const Team& team, const Problem& P, const Frame& F
 // contact-free frame: exact selector elimination + 3 refinement rounds
 // (solver.py:388-421).  Writes ws.dx and ws.yfull[0..nf).
 template <class Team>
-DEVNI int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res) {
+DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res) {
   const int N = P.m.N, n = 6 * N;
   if (reduced_factor(team, P, 0.0, ws) >= 0) return ST_LINALG;
   eliminated_rhs(team, P, F, ws, ws.rhs);
@@ -380,7 +380,7 @@ DEVNI int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& w
 
 // dense Cholesky + solve of the na x na Schur complement (row-major, ld = na)
 template <class Team>
-DEVNI bool dense_chol(const Team& team, int na, double* S) {
+DEV bool dense_chol(const Team& team, int na, double* S) {
   for (int k = 0; k < na; ++k) {
     double piv = S[k * na + k];
     if (!(piv > 0.0)) return false;
@@ -402,7 +402,7 @@ DEVNI bool dense_chol(const Team& team, int na, double* S) {
 }
 
 template <class Team>
-DEVNI void dense_solve(const Team& team, int na, const double* S, double* b) {
+DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
   for (int k = 0; k < na; ++k) {
     team.sync();
     double bk = b[k] / S[k * na + k];
@@ -444,7 +444,7 @@ DEV void dense_combine(const Team& team, int n, int na, const int* alist, const 
 }
 
 template <class Team>
-DEVNI int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
+DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
   const int N = P.m.N, n = 6 * N, nf = F.nf, nc = F.nc;
   const double tol_act = fmax(10.0 * P.s.eps_abs, 1e-12);
   const double delta = 1e-9;
@@ -607,7 +607,7 @@ DEVNI int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpR
 // taken from ws.warm (by node) and ws.wfix.  On return ws.dx, ws.yfull.
 // ---------------------------------------------------------------------------
 template <class Team>
-DEVNI int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, double rho_in, int has_wfix,
+DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, double rho_in, int has_wfix,
                  QpResult& res, int cmax) {
   const Settings& S = P.s;
   const int N = P.m.N, n = 6 * N, nf = F.nf, m = F.m;
