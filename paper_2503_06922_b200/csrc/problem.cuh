@@ -108,10 +108,10 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   // hot: the factor (packed symmetric diagonal blocks, full couplings) and the solve vectors
   w.HD = takeh(22L * N); w.HU = takeh(36 * E);
   w.rhs = takeh(n); w.tmp = takeh(n); w.xs = takeh(n); w.gs = takeh(n);
+  w.z = takeh(m); w.y = takeh(m); w.rho = takeh(m); w.ls = takeh(m); w.us = takeh(m); w.as = takeh(3 * m);
   w.xt = w.rhs;  // the solve writes its result over the right-hand side
   // cold
-  w.z = take(m); w.y = take(m); w.yprev = take(m); w.rho = take(m); w.ls = take(m); w.us = take(m);
-  w.tr = take(m); w.as = take(3 * m);
+  w.yprev = take(m); w.tr = take(m);
   w.R = take(9L * N); w.frames = take(9 * E); w.fe = take(12 * E); w.ke = take(108 * E);
   w.fint = take(n); w.KD = take(36L * N); w.KU = take(36 * E);
   w.fa = take(n); w.g = take(n); w.rres = take(n);
@@ -147,10 +147,9 @@ HDEV long ws_doubles(int N, int nf, int cmax_polish) {
 
 // hot-region size (doubles) of one team
 HDEV long ws_hot_doubles(int N, int nf) {
-  long n = 6L * N;
-  (void)nf;
+  long n = 6L * N, m = (long)nf + N;
   auto r2 = [](long k) { return (k + 1) & ~1L; };
-  return r2(22L * N) + r2(36L * (N - 1)) + 4 * r2(n);
+  return r2(22L * N) + r2(36L * (N - 1)) + 4 * r2(n) + 5 * r2(m) + r2(3 * m);
 }
 
 // ---------------------------------------------------------------------------

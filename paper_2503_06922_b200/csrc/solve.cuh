@@ -115,10 +115,43 @@ DEV double hcol_max(const double* HD, const double* HU, int N, int j) {
   return mx;
 }
 
+// max_i |H_ij| d_i over the 18 stored entries of column j (unscaled H in HD/HU)
+DEV double hcol_wmax(const double* HD, const double* HU, const double* d, int N, int j) {
+  const int k = j / 6, cc = j % 6;
+  double mx = 0.0;
+  const double* dk = HD + kDiag * k;
+  const double* wk = d + 6 * k;
+#pragma unroll
+  for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(dk[sidx(r, cc)]) * wk[r]);
+  if (k + 1 < N) {
+    const double* u = HU + 36 * k + 6 * cc;  // block (k+1, k) = U_k^T: column cc holds U_k row cc
+    const double* wn = d + 6 * (k + 1);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(u[r]) * wn[r]);
+  }
+  if (k > 0) {
+    const double* u = HU + 36 * (k - 1) + cc;
+    const double* wp = d + 6 * (k - 1);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) mx = fmax(mx, fabs(u[6 * r]) * wp[r]);
+  }
+  return mx;
+}
+
+// Modified Ruiz equilibration of [[H, A^T], [A, 0]] + cost scaling
+// (solver.py:169-212).  The reference rescales every stored entry each
+// sweep; here H stays unscaled and the sweeps only carry the diagonal
+// scalings d, e and the cost factor c (the scaled column maximum of column j
+// is c d_j max_i |H_ij| d_i), so each sweep is one column pass; the scaled
+// matrix H_s = c D H D and A_s = E A D are formed once at the end.  The
+// result equals the reference's up to rounding.
 template <class Team>
 DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   const int N = P.m.N, n = 6 * N, E = N - 1;
   const int nf = F.nf, m = F.m;
+  double* d = ws.tmp;   // hot scratch until the ADMM loop: the running column scaling
+  double* hw = ws.colh; // per column: max_i |H_ij| d_i for the current d
+  double* dd = ws.v;    // this sweep's column factors
   PARFOR(i, 21 * N) {
     int k = i / 21, p = i - 21 * k, r, c;
     sym_rc(p, r, c);
@@ -127,7 +160,7 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   parfor4(team, 36 * E, [&](int i) { ws.HU[i] = ws.KU[i]; });
   parfor4(team, n, [&](int j) {
     ws.gs[j] = ws.g[j];
-    ws.d[j] = 1.0;
+    d[j] = 1.0;
   });
   PARFOR(r, m) {
     ws.e[r] = 1.0;
@@ -141,75 +174,76 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
     }
   }
   team.sync();
+  parfor4(team, n, [&](int j) { hw[j] = hcol_wmax(ws.HD, ws.HU, d, N, j); });
+  team.sync();
   double c = 1.0;
-  double* dd = ws.tmp;  // hot scratch: unused until the ADMM loop
   double* ee = ws.tr;
-  double gam_prev = 1.0;
-  double* colg = ws.colh;  // column maxima of H from the previous sweep's cost pass
   for (int sweep = 0; sweep < P.s.scaling_iterations; ++sweep) {
+    // column factors from the scaled KKT column maxima (H part and A part)
     PARFOR(j, n) {
-      // H part: max |gam h| = gam * max |h| exactly (rounding is monotone), so
-      // sweeps after the first reuse the previous cost-normalisation pass
-      double mx = sweep == 0 ? hcol_max(ws.HD, ws.HU, N, j) : gam_prev * colg[j];
-      int fr = P.m.fixed_row_of_dof[j];
-      if (fr >= 0) mx = fmax(mx, fabs(ws.as[3 * fr]));
-      int cc = j % 6;
+      double mx = c * d[j] * hw[j];
+      const int fr = P.m.fixed_row_of_dof[j];
+      if (fr >= 0) mx = fmax(mx, ws.e[fr] * fabs(ws.as[3 * fr]) * d[j]);
+      const int cc = j % 6;
       if (cc < 3) {
-        int ct = ws.crow_of_node[j / 6];
-        if (ct >= 0) mx = fmax(mx, fabs(ws.as[3 * (nf + ct) + cc]));
+        const int ct = ws.crow_of_node[j / 6];
+        if (ct >= 0) mx = fmax(mx, ws.e[nf + ct] * fabs(ws.as[3 * (nf + ct) + cc]) * d[j]);
       }
       dd[j] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
     }
     PARFOR(r, m) {
-      double mx = fabs(ws.as[3 * r]);
-      if (r >= nf) mx = fmax(mx, fmax(fabs(ws.as[3 * r + 1]), fabs(ws.as[3 * r + 2])));
+      double mx;
+      if (r < nf) {
+        mx = ws.e[r] * fabs(ws.as[3 * r]) * d[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
+      } else {
+        const int nd = ws.cnode[r - nf];
+        mx = fmax(fmax(fabs(ws.as[3 * r]) * d[6 * nd], fabs(ws.as[3 * r + 1]) * d[6 * nd + 1]),
+                  fabs(ws.as[3 * r + 2]) * d[6 * nd + 2]) * ws.e[r];
+      }
       ee[r] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
     }
     team.sync();
-    parfor4(team, 21 * N, [&](int i) {
-      int k = i / 21, p = i - 21 * k, r, cc;
-      sym_rc(p, r, cc);
-      ws.HD[kDiag * k + p] *= dd[6 * k + r] * dd[6 * k + cc];
-    });
-    parfor4(team, 36 * E, [&](int i) {
-      int k = i / 36, t = i - 36 * k, r = t / 6, cc = t - 6 * r;
-      ws.HU[i] *= dd[6 * k + r] * dd[6 * (k + 1) + cc];
-    });
-    PARFOR(r, m) {
-      if (r < nf) {
-        ws.as[3 * r] *= ee[r] * dd[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
-      } else {
-        int nd = ws.cnode[r - nf];
-        for (int q = 0; q < 3; ++q) ws.as[3 * r + q] *= ee[r] * dd[6 * nd + q];
-      }
-      ws.e[r] *= ee[r];
-    }
     parfor4(team, n, [&](int j) {
+      d[j] *= dd[j];
       ws.gs[j] *= dd[j];
-      ws.d[j] *= dd[j];
     });
+    PARFOR(r, m) ws.e[r] *= ee[r];
     team.sync();
-    // cost normalisation: column maxima of the scaled H only
+    // cost normalisation on the column maxima of the new scaled H
     double csum = 0.0, gmax = 0.0;
     PARFOR(j, n) {
-      const double cm = hcol_max(ws.HD, ws.HU, N, j);
-      colg[j] = cm;
-      csum += cm;
+      const double w = hcol_wmax(ws.HD, ws.HU, d, N, j);
+      hw[j] = w;
+      csum += c * d[j] * w;
       gmax = fmax(gmax, fabs(ws.gs[j]));
     }
     csum = team.sum(csum);
     gmax = team.max(gmax);
-    double gam = 1.0 / fmax(fmax(csum / n, gmax), 1e-12);
-    gam_prev = gam;
-    parfor4(team, 21 * N, [&](int i) {
-      int k = i / 21;
-      ws.HD[kDiag * k + (i - 21 * k)] *= gam;
-    });
-    parfor4(team, 36 * E, [&](int i) { ws.HU[i] *= gam; });
+    const double gam = 1.0 / fmax(fmax(csum / n, gmax), 1e-12);
     parfor4(team, n, [&](int j) { ws.gs[j] *= gam; });
     c *= gam;
     team.sync();
   }
+  // materialise H_s = c D H D, A_s = E A D; keep d for the unscaling
+  parfor4(team, 21 * N, [&](int i) {
+    int k = i / 21, p = i - 21 * k, r, cc;
+    sym_rc(p, r, cc);
+    ws.HD[kDiag * k + p] *= c * (d[6 * k + r] * d[6 * k + cc]);
+  });
+  parfor4(team, 36 * E, [&](int i) {
+    int k = i / 36, t = i - 36 * k, r = t / 6, cc = t - 6 * r;
+    ws.HU[i] *= c * (d[6 * k + r] * d[6 * (k + 1) + cc]);
+  });
+  PARFOR(r, m) {
+    if (r < nf) {
+      ws.as[3 * r] *= ws.e[r] * d[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]];
+    } else {
+      const int nd = ws.cnode[r - nf];
+      for (int q = 0; q < 3; ++q) ws.as[3 * r + q] *= ws.e[r] * d[6 * nd + q];
+    }
+  }
+  parfor4(team, n, [&](int j) { ws.d[j] = d[j]; });
+  team.sync();
   return c;
 }
 
