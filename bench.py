@@ -321,6 +321,23 @@ def main():
                "path": "Engine.solve_static_batch(numpy) -> accfem_solve_batch_host: H2D from pinned host "
                        "buffers, solve, D2H of every output"}
 
+    # p50 single-solve latency (batch = 1, wall clock incl. launch and sync)
+    lat = {}
+    if rank == 0:
+        for tag, wl in (("cfg4_s0", scenarios.cfg4(1, start=start)), ("cfg3p", scenarios.cfg3p(1))):
+            e1 = eng if tag == "cfg4_s0" else Engine(**wl.engine_kwargs(), device=local)
+            a = [None if v is None else torch.tensor(v, device=dev) for v in (wl.x0, wl.tensions, wl.applied)]
+            o1 = e1.allocate_batch(1)
+            ts = []
+            for rep in range(12):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                e1.solve_static_batch(a[0], a[1], a[2], tol=wl.tol, max_frames=wl.max_frames, out=o1)
+                torch.cuda.synchronize()
+                if rep >= 2:
+                    ts.append((time.perf_counter() - t0) * 1e3)
+            lat[tag] = {"p50_ms": statistics.median(ts), "frames": int(o1.frames[0].item())}
+
     line = None
     if rank == 0:
         fl = flops_per_solve(eng, w)
@@ -350,6 +367,7 @@ def main():
                                         "MEASURED_PEAKS.json)",
                          "flop_per_solve": fl, "kernel": "k_solve (persistent, one warp per scenario)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "latency": {"batch": 1, "wall_clock": "solve_static_batch + cudaDeviceSynchronize", **lat},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

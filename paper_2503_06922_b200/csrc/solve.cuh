@@ -490,7 +490,10 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     ws.act[c] = (yc > tol_act) || (slack < tol_act);
   }
   team.sync();
+  PROF_T0(t_pf);
   if (reduced_factor(team, P, delta, ws) >= 0) return ST_OK;  // splu failure -> no polish
+  PROF_ADD(ws, PF_POL_FACTOR, t_pf);
+  PROF_T0(t_pw);
   // W_c = P^{-1} C~_c, 16 contacts per warp pass (C~: contact row with selector DOFs zeroed)
   for (int c0 = 0; c0 < nc; c0 += kMultiRhs) {
     const int nb = nc - c0 < kMultiRhs ? nc - c0 : kMultiRhs;
@@ -525,6 +528,8 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
   double* yp = ws.yp;
   double* yact = ws.Sy + cmax;      // na entries
   double* dyq = ws.Sy + 2 * cmax;   // na entries
+  PROF_ADD(ws, PF_POL_W, t_pw);
+  PROF_T0(t_pr);
   for (int round = 0; round < 6; ++round) {
     // active contact list in row order
     int na = 0;
@@ -609,6 +614,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     }
     team.sync();
   }
+  PROF_ADD(ws, PF_POL_ROUNDS, t_pr);
   if (!found) return ST_OK;
   // acceptance (solver.py:483-497)
   double pri = 0.0, fin = 1.0;

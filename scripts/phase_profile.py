@@ -26,4 +26,5 @@ print(f"{name} S={S} wall {dt*1e3:.1f} ms -> {S/dt:.0f} solves/s; frames/solve {
 for i, nm in enumerate(names[:11]):
     print(f"  {nm:10s} {p[i]/S/1e6:9.3f} Mcycles/solve  {100*p[i]/max(p[10],1):5.1f}%")
 print(f"  per ADMM iteration: {p[4]/max(p[11],1):.0f} cycles (chain {p[5]/max(p[11],1):.0f})")
+print(f"  polish: factor {p[13]/S/1e6:.3f} W+S+v {p[14]/S/1e6:.3f} rounds {p[15]/S/1e6:.3f} Mcycles/solve")
 print(f"  per frame: element {p[0]/max(p[12],1):.0f} detect {p[1]/max(p[12],1):.0f} ruiz {p[2]/max(p[12],1):.0f} factor {p[3]/max(p[12],1):.0f} polish {p[7]/max(p[12],1):.0f}")
