@@ -160,7 +160,8 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
     ws.yp[r] = y * fac;
   }
   team.sync();
-  PARFOR(j, n) ws.rres[j] = col_dot(P, F, ws, j, ws.yp) - ws.fa[j];
+  at_y(team, P, F, ws, ws.yp, ws.rres);
+  parfor4(team, n, [&](int j) { ws.rres[j] -= ws.fa[j]; });
   team.sync();
   pending = true;
   PROF_ADD(ws, PF_POST, t_post);

@@ -290,6 +290,39 @@ DEV void twisted_solve_multi(const TeamSerial& t, int N, const double* D, const 
   twisted_solve(t, N, D, U, rhs, tmp, out, nrhs, stride);
 }
 
+DEV int q_per_half(int N) {
+  const int k = twist_split(N);
+  const int K = k > N - 1 - k ? k : N - 1 - k;
+  return (K + 1) / 2;
+}
+
+// Q(t) and Q(t)^T for odd t in [1, K-1] of both halves -> Qg[2][half][QH][36]
+template <class Team>
+DEV void twisted_q(const Team& team, int N, const double* U, double* Qg) {
+  const int k = twist_split(N);
+  const int QH = q_per_half(N);
+  PARFOR(i, 2 * QH * 36) {
+    const int h = i / (QH * 36), rem = i - h * QH * 36, qi = rem / 36, e = rem - 36 * qi;
+    const int K = h == 0 ? k : N - 1 - k;
+    const int t = 2 * qi + 1;
+    if (t > K - 1) continue;
+    const double* M1 = U + 36 * (h == 0 ? k - t - 1 : k + t);
+    const double* M2 = U + 36 * (h == 0 ? k - t : k + t - 1);
+    const int r = e / 6, c = e - 6 * r;
+    double a = 0.0;
+    for (int q = 0; q < 6; ++q) a += M2[6 * r + q] * M1[6 * q + c];
+    Qg[(h * QH + qi) * 36 + e] = a;                      // Q
+    Qg[(2 * QH + h * QH + qi) * 36 + 6 * c + r] = a;     // Q^T
+  }
+  team.sync();
+}
+
+DEV void twisted_solve_la(const TeamSerial& t, int N, const double* D, const double* U, const double* Qg, double* rhs,
+                          double* tmp, double* out, bool sh) {
+  (void)Qg;
+  twisted_solve(t, N, D, U, rhs, tmp, out, 1, 0, sh);
+}
+
 #if defined(__CUDACC__)
 // Warp factorisation: lane 0 runs the top recursion, lane 1 the bottom one,
 // each 6x6 step entirely in registers; they meet at the middle block.
@@ -498,6 +531,206 @@ DEV void twisted_solve(const TeamWarp& team, int N, const double* D, const doubl
   else twisted_solve_impl<false, false>(team, N, D, U, rhs, tmp, out);
 }
 
+// ---------------------------------------------------------------------------
+// Two-blocks-per-step ("look-ahead") variant of the single-RHS solve.
+//
+// Per half, index blocks by their distance t from the middle block k (top:
+// block k-t, bottom: block k+t; K = blocks in the half).  With
+//   M1(t) = coupling of the sweep-1 step into distance t  (top X_{k-t}, bottom Y_{k+t}),
+//   M2(t) = coupling of the sweep-2 step into distance t  (top X_{k-t+1}, bottom Y_{k+t-1}),
+// and Q(t) = M2(t) M1(t) for odd t (stored by twisted_q, plus its transpose),
+// sweep 1 computes two blocks from one source:   v(s-1) = b(s-1) - M1(s-1) v(s),
+//   v(s-2) = c(s-2) + Q(s-1) v(s),  c(s-2) = b(s-2) - M1(s-2) b(s-1),
+// and sweep 2 likewise outward:                  x(s+1) = z(s+1) - M2(s+1)^T x(s),
+//   x(s+2) = c'(s+2) + Q(s+1)^T x(s),  c'(s+2) = z(s+2) - M2(s+2)^T z(s+1).
+// The c / c' terms are independent of the recurrence and are formed for all
+// blocks in parallel first, so each dependent step still costs one 6-wide
+// shuffle mat-vec but advances two blocks.  Lanes 0-11 run the top half,
+// 12-23 the bottom half; within a half lanes 0-5 produce the near block and
+// lanes 6-11 the far block of a step.
+// ---------------------------------------------------------------------------
+DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// Look-ahead solve for odd N (both halves have K = k blocks, so the two
+// halves run identical schedules and the loops carry no predicates).
+template <bool SH>
+DEV void twisted_solve_la_impl(const TeamWarp& team, int N, const double* __restrict__ D,
+                               const double* __restrict__ U, const double* __restrict__ Qg, double* rhs,
+                               double* tmp, double* out) {
+  if (SH) {
+    __builtin_assume(__isShared(D));
+    __builtin_assume(__isShared(U));
+    __builtin_assume(__isShared(rhs));
+    __builtin_assume(__isShared(tmp));
+    __builtin_assume(__isShared(out));
+  }
+  const int lane = team.lane;
+  const int h = (lane >= 12 && lane < 24) ? 1 : 0;  // lanes 24-31 shadow the top half
+  const int g = (lane % 12) / 6, r = lane % 6;
+  const bool act = lane < 24;
+  const int k = twist_split(N), K = k;  // N odd: N - 1 - k == k
+  const int QH = q_per_half(N);
+  const int sg = h == 0 ? -1 : 1;       // block(t) = k + sg t
+  const bool hasA = (K & 1) && K > 1;
+  const int s0 = K - (hasA ? 1 : 0);
+  const int P1 = s0 >= 4 ? (s0 - 2) / 2 : 0;
+  const bool hasB = s0 >= 2;
+  const int P2 = K / 2;
+  const bool hasC = K & 1;
+  // ---- c(t) = b(t) - M1(t) b(t+1), even t in [2, s0-2] of both halves (M1(t) = U[k-t-1] / U[k+t])
+  for (int q = lane; q < 12 * P1; q += 32) {
+    const int hh = q >= 6 * P1 ? 1 : 0;
+    const int qq = q - 6 * P1 * hh;
+    const int t = 2 + 2 * (qq / 6), rr = qq - 6 * (qq / 6);
+    const int s2 = hh == 0 ? -1 : 1;
+    const double* M = U + 36 * (hh == 0 ? k - t - 1 : k + t) + 6 * rr;
+    const double* bn = rhs + 6 * (k + s2 * (t + 1));
+    rhs[6 * (k + s2 * t) + rr] -=
+        (M[0] * bn[0] + M[2] * bn[2] + M[4] * bn[4]) + (M[1] * bn[1] + M[3] * bn[3] + M[5] * bn[5]);
+  }
+  __syncwarp();
+  // ---- sweep 1 (toward the middle); the source block is held by lane group gsrc
+  int gsrc = 0;
+  double cur = rhs[6 * (k + sg * K) + r];
+  if (act && g == 0) tmp[6 * (k + sg * K) + r] = cur;
+  double p[6];
+  auto fetch = [&]() {
+    const int b = 12 * h + 6 * gsrc;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) p[j] = __shfl_sync(0xffffffffu, cur, b + j);
+  };
+  auto dot6 = [&](const double* M, int st) {
+    return (M[0] * p[0] + M[2 * st] * p[2] + M[4 * st] * p[4]) + (M[st] * p[1] + M[3 * st] * p[3] + M[5 * st] * p[5]);
+  };
+  if (hasA) {  // distance K-1 from K: M1(K-1) = U[k-K] / U[k+K-1]
+    const double* M = U + 36 * (h == 0 ? k - K : k + K - 1) + 6 * r;
+    const double a0 = rhs[6 * (k + sg * (K - 1)) + r];
+    fetch();
+    const double a = a0 - dot6(M, 1);
+    if (g == 0) {
+      cur = a;
+      if (act) tmp[6 * (k + sg * (K - 1)) + r] = a;
+    }
+  }
+  if (P1 > 0) {
+    // near block s-1 (group 0): M1(s-1) row; far block s-2 (group 1): Q(s-1) row
+    const double* Mp = g == 0 ? U + 36 * (h == 0 ? k - s0 : k + s0 - 1) + 6 * r
+                              : Qg + (h * QH + (s0 - 2) / 2) * 36 + 6 * r;
+    const int dM = g == 0 ? (h == 0 ? 72 : -72) : -36;
+    const int tb0 = g == 0 ? s0 - 1 : s0 - 2;
+    const double* ap = rhs + 6 * (k + sg * tb0) + r;
+    double* vp = tmp + 6 * (k + sg * tb0) + r;
+    const int db = h == 0 ? 12 : -12;
+    for (int pi = 0; pi < P1; ++pi) {
+      const double m0 = Mp[0], m1 = Mp[1], m2 = Mp[2], m3 = Mp[3], m4 = Mp[4], m5 = Mp[5];
+      const double a0 = *ap;
+      fetch();
+      const double d = (m0 * p[0] + m2 * p[2] + m4 * p[4]) + (m1 * p[1] + m3 * p[3] + m5 * p[5]);
+      cur = g == 0 ? a0 - d : a0 + d;
+      if (act) *vp = cur;
+      gsrc = 1;
+      Mp += dM;
+      ap += db;
+      vp += db;
+    }
+  }
+  if (hasB) {  // distance 1 from 2: M1(1) = U[k-2] / U[k+1]
+    const double* M = U + 36 * (h == 0 ? k - 2 : k + 1) + 6 * r;
+    const double a0 = rhs[6 * (k + sg) + r];
+    fetch();
+    const double a = a0 - dot6(M, 1);
+    if (g == 0) {
+      cur = a;
+      if (act) tmp[6 * (k + sg) + r] = a;
+    }
+    gsrc = 0;
+  }
+  // ---- middle: x_k = Zinv (b_k - (X_k v_{k-1} + Y_k u_{k+1})); M2(1) = U[k-1] / U[k]
+  double part;
+  {
+    const double* M = U + 36 * (h == 0 ? k - 1 : k) + 6 * r;
+    fetch();
+    part = K >= 1 ? (M[0] * p[0] + M[1] * p[1] + M[2] * p[2] + M[3] * p[3] + M[4] * p[4] + M[5] * p[5]) : 0.0;
+  }
+  const double opart = __shfl_sync(0xffffffffu, part, (h == 0 ? 12 : 0) + 6 * g + r);
+  const double tk = rhs[6 * k + r] - ((h == 0 ? part : opart) + (h == 0 ? opart : part));
+  double xk;
+  {
+    const double* Dk = D + kDiag * k;
+    const double d0 = Dk[sidx(r, 0)], d1 = Dk[sidx(r, 1)], d2 = Dk[sidx(r, 2)];
+    const double d3 = Dk[sidx(r, 3)], d4 = Dk[sidx(r, 4)], d5 = Dk[sidx(r, 5)];
+    const int b = 12 * h + 6 * g;
+    double q[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) q[j] = __shfl_sync(0xffffffffu, tk, b + j);
+    xk = (d0 * q[0] + d2 * q[2] + d4 * q[4]) + (d1 * q[1] + d3 * q[3] + d5 * q[5]);
+  }
+  __syncwarp();  // sweep-1 values visible
+  // ---- z_i = Dinv_i v_i for every block but k (parked in out)
+  parfor4(team, 6 * N, [&](int q) {
+    const int i = q / 6, rr = q - 6 * i;
+    if (i != k) {
+      const double* Di = D + kDiag * i;
+      const double* vi = tmp + 6 * i;
+      out[q] = (Di[sidx(rr, 0)] * vi[0] + Di[sidx(rr, 2)] * vi[2] + Di[sidx(rr, 4)] * vi[4]) +
+               (Di[sidx(rr, 1)] * vi[1] + Di[sidx(rr, 3)] * vi[3] + Di[sidx(rr, 5)] * vi[5]);
+    }
+  });
+  __syncwarp();
+  // ---- c'(t) = z(t) - M2(t)^T z(t-1), even t in [2, K] (M2(t) = U[k-t] / U[k+t-1])
+  for (int q = lane; q < 12 * P2; q += 32) {
+    const int hh = q >= 6 * P2 ? 1 : 0;
+    const int qq = q - 6 * P2 * hh;
+    const int t = 2 + 2 * (qq / 6), rr = qq - 6 * (qq / 6);
+    const int s2 = hh == 0 ? -1 : 1;
+    const double* Mc = U + 36 * (hh == 0 ? k - t : k + t - 1) + rr;
+    const double* zn = out + 6 * (k + s2 * (t - 1));
+    out[6 * (k + s2 * t) + rr] -=
+        (Mc[0] * zn[0] + Mc[12] * zn[2] + Mc[24] * zn[4]) + (Mc[6] * zn[1] + Mc[18] * zn[3] + Mc[30] * zn[5]);
+  }
+  __syncwarp();
+  if (h == 0 && g == 0 && act) out[6 * k + r] = xk;
+  // ---- sweep 2 (outward): near s+1 (group 0): column r of M2(s+1); far s+2 (group 1): row r of Q(s+1)^T
+  cur = xk;
+  gsrc = 0;
+  if (P2 > 0) {
+    const double* Mp = g == 0 ? U + 36 * (h == 0 ? k - 1 : k) + r : Qg + (2 * QH + h * QH) * 36 + 6 * r;
+    const int st = g == 0 ? 6 : 1;
+    const int dM = g == 0 ? (h == 0 ? -72 : 72) : 36;
+    const int tb0 = g == 0 ? 1 : 2;
+    double* op = out + 6 * (k + sg * tb0) + r;
+    const int db = h == 0 ? -12 : 12;
+    for (int pi = 0; pi < P2; ++pi) {
+      const double m0 = Mp[0], m1 = Mp[st], m2 = Mp[2 * st], m3 = Mp[3 * st], m4 = Mp[4 * st], m5 = Mp[5 * st];
+      const double a0 = *op;
+      fetch();
+      const double d = (m0 * p[0] + m2 * p[2] + m4 * p[4]) + (m1 * p[1] + m3 * p[3] + m5 * p[5]);
+      cur = g == 0 ? a0 - d : a0 + d;
+      if (act) *op = cur;
+      gsrc = 1;
+      Mp += dM;
+      op += db;
+    }
+  }
+  if (hasC) {  // distance K (odd) from K-1: column r of M2(K) = U[k-K] / U[k+K-1]
+    const double* Mc = U + 36 * (h == 0 ? k - K : k + K - 1) + r;
+    const double a0 = out[6 * (k + sg * K) + r];
+    fetch();
+    const double a = a0 - dot6(Mc, 6);
+    if (g == 0 && act) out[6 * (k + sg * K) + r] = a;
+  }
+  __syncwarp();
+}
+
+DEV void twisted_solve_la(const TeamWarp& team, int N, const double* D, const double* U, const double* Qg,
+                          double* rhs, double* tmp, double* out, bool sh) {
+  if (!(N & 1)) {  // even N: the halves differ by one block; use the one-block-per-step solve
+    twisted_solve(team, N, D, U, rhs, tmp, out, 1, 0, sh, sh);
+    return;
+  }
+  if (sh) twisted_solve_la_impl<true>(team, N, D, U, Qg, rhs, tmp, out);
+  else twisted_solve_la_impl<false>(team, N, D, U, Qg, rhs, tmp, out);
+}
 // Many right-hand sides (g < 16): lanes 2g / 2g+1 sweep the top / bottom half
 // of RHS g with the full 6x6 mat-vec in registers; the z_i = Dinv_i v_i
 // products run across all lanes between the sweeps.  out may alias rhs.

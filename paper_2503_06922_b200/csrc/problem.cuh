@@ -80,7 +80,7 @@ struct Ws {
   // scaled system; HD/HU hold H_s, then M, then its twisted factor in place
   double *HD, *HU, *gs, *d, *colh, *xs, *xt, *rhs, *w, *v, *tmp;
   // solution / polish
-  double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr, *W, *Sf, *Cv;
+  double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr, *W, *Sf, *Cv, *Qg;
   int *act, *alist;
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
   bool sh;                   // hot arrays live in shared memory
@@ -123,6 +123,7 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   w.W = take(cp * n);      // polish: P^{-1} C~_c for every contact c
   w.Sf = take(cp * cp);    // polish: C P^{-1} C~^T over all contacts
   w.Cv = take(cp);
+  w.Qg = take(4L * ((N + 1) / 2 + 1) * 36);  // look-ahead products Q and Q^T of both halves
   w.wfix = take(n);
   w.scr = take(160);
   double* ib = take((5L * N + m + 8) / 2 + 1);

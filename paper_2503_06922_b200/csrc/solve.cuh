@@ -84,6 +84,27 @@ DEV double col_dot(const Problem& P, const Frame& F, const Ws& ws, int j, const 
   return acc;
 }
 
+// out = A^T y with unscaled rows, as two conflict-free row passes (selector
+// rows hit distinct DOFs, contact rows distinct nodes) instead of a per-DOF
+// gather through the row-lookup tables
+template <class Team>
+DEV void at_y(const Team& team, const Problem& P, const Frame& F, const Ws& ws, const double* y, double* out) {
+  const int n = 6 * P.m.N;
+  parfor4(team, n, [&](int j) { out[j] = 0.0; });
+  team.sync();
+  PARFOR(r, F.nf) out[6 * P.m.fixed_node[r] + P.m.fixed_dof[r]] += y[r];
+  team.sync();
+  PARFOR(c, F.nc) {
+    const double yc = y[F.nf + c];
+    double* o = out + 6 * ws.cnode[c];
+    const double* nr = ws.cnrm + 3 * c;
+    o[0] += nr[0] * yc;
+    o[1] += nr[1] * yc;
+    o[2] += nr[2] * yc;
+  }
+  team.sync();
+}
+
 // ---------------------------------------------------------------------------
 // modified Ruiz equilibration of [[H, A^T], [A, 0]] + cost scaling
 // (solver.py:169-212).  Produces HD/HU (scaled H), as (scaled rows), gs, d,
@@ -179,18 +200,24 @@ DEV double ruiz(const Team& team, const Problem& P, const Frame& F, Ws& ws) {
   double c = 1.0;
   double* ee = ws.tr;
   for (int sweep = 0; sweep < P.s.scaling_iterations; ++sweep) {
-    // column factors from the scaled KKT column maxima (H part and A part)
-    PARFOR(j, n) {
-      double mx = c * d[j] * hw[j];
-      const int fr = P.m.fixed_row_of_dof[j];
-      if (fr >= 0) mx = fmax(mx, ws.e[fr] * fabs(ws.as[3 * fr]) * d[j]);
-      const int cc = j % 6;
-      if (cc < 3) {
-        const int ct = ws.crow_of_node[j / 6];
-        if (ct >= 0) mx = fmax(mx, ws.e[nf + ct] * fabs(ws.as[3 * (nf + ct) + cc]) * d[j]);
-      }
-      dd[j] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
+    // column factors from the scaled KKT column maxima: H part, then the A
+    // part scattered row by row (selector rows, then contact rows)
+    parfor4(team, n, [&](int j) { dd[j] = c * d[j] * hw[j]; });
+    team.sync();
+    PARFOR(r, nf) {
+      const int j = 6 * P.m.fixed_node[r] + P.m.fixed_dof[r];
+      dd[j] = fmax(dd[j], ws.e[r] * fabs(ws.as[3 * r]) * d[j]);
     }
+    team.sync();
+    PARFOR(ct, m - nf) {
+      const int r = nf + ct, j0 = 6 * ws.cnode[ct];
+      for (int q = 0; q < 3; ++q) dd[j0 + q] = fmax(dd[j0 + q], ws.e[r] * fabs(ws.as[3 * r + q]) * d[j0 + q]);
+    }
+    team.sync();
+    parfor4(team, n, [&](int j) {
+      const double mx = dd[j];
+      dd[j] = 1.0 / sqrt(mx > 1e-12 ? mx : 1.0);
+    });
     PARFOR(r, m) {
       double mx;
       if (r < nf) {
@@ -270,13 +297,13 @@ DEV Residuals unscaled_residuals(const Team& team, const Problem& P, const Frame
     ps = fmax(ps, fmax(fabs(ax), fabs(zu)));
   }
   block_matvec(team, N, ws.KD, ws.KU, xu, ws.v);  // includes sync
+  at_y(team, P, F, ws, ws.yfull, ws.w);
   double dua = 0.0, ds = 0.0;
-  PARFOR(j, n) {
-    double hx = ws.v[j];
-    double aty = col_dot(P, F, ws, j, ws.yfull);
+  parfor4(team, n, [&](int j) {
+    const double hx = ws.v[j], aty = ws.w[j];
     dua = fmax(dua, fabs(hx + ws.g[j] + aty));
     ds = fmax(ds, fmax(fabs(hx), fabs(aty)));
-  }
+  });
   Residuals R;
   R.pri = team.max(pri);
   R.ps = team.max(ps);
@@ -309,8 +336,9 @@ DEV bool infeasible(const Team& team, const Problem& P, const Frame& F, Ws& ws, 
   double support = team.sum(sup_u) + team.sum(sup_l);
   team.sync();
   if (!(support < -eps)) return false;
+  at_y(team, P, F, ws, ws.tr, ws.w);
   double at = 0.0;
-  PARFOR(j, n) at = fmax(at, fabs(col_dot(P, F, ws, j, ws.tr)));
+  parfor4(team, n, [&](int j) { at = fmax(at, fabs(ws.w[j])); });
   at = team.max(at);
   return at <= eps;
 }
@@ -403,7 +431,8 @@ DEV int direct_solve(const Team& team, const Problem& P, const Frame& F, Ws& ws,
   selector_multipliers(team, P, F, ws, ws.dx, ws.yfull);
   double dua = 0.0;
   block_matvec(team, N, ws.KD, ws.KU, ws.dx, ws.tmp);
-  PARFOR(j, n) dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + col_dot(P, F, ws, j, ws.yfull)));
+  at_y(team, P, F, ws, ws.yfull, ws.w);
+  parfor4(team, n, [&](int j) { dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + ws.w[j])); });
   res.pri = 0.0;
   res.dua = team.max(dua);
   res.iterations = 0;
@@ -624,11 +653,12 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     if (r < nf) pri = fmax(pri, fabs(ax - ws.up[r]));
   }
   block_matvec(team, N, ws.KD, ws.KU, dxp, ws.tmp);
+  at_y(team, P, F, ws, yp, ws.w);
   double dua = 0.0;
-  PARFOR(j, n) {
-    dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + col_dot(P, F, ws, j, yp)));
+  parfor4(team, n, [&](int j) {
+    dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + ws.w[j]));
     if (!isfinite(dxp[j])) fin = 0.0;
-  }
+  });
   pri = team.max(pri);
   dua = team.max(dua);
   fin = team.min(fin);
@@ -671,30 +701,30 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     ws.us[r] = ws.e[r] * ws.up[r];
   }
   team.sync();
-  // M = H_s + sigma I + A_s^T diag(rho) A_s  (packed diagonal blocks; HU holds H_s off-diagonal)
-  PARFOR(i, 21 * N) {
-    int k = i / 21, p = i - 21 * k, r, cc;
-    sym_rc(p, r, cc);
-    double v = ws.HD[kDiag * k + p];
-    if (r == cc) {
-      v += S.sigma;
-      int fr = P.m.fixed_row_of_dof[6 * k + r];
-      if (fr >= 0) v += ws.rho[fr] * ws.as[3 * fr] * ws.as[3 * fr];
-    }
-    if (r < 3 && cc < 3) {
-      int ct = ws.crow_of_node[k];
-      if (ct >= 0) {
-        int row = nf + ct;
-        v += ws.rho[row] * ws.as[3 * row + r] * ws.as[3 * row + cc];
-      }
-    }
-    ws.HD[kDiag * k + p] = v;
+  // M = H_s + sigma I + A_s^T diag(rho) A_s  (packed diagonal blocks; HU holds H_s off-diagonal):
+  // sigma on the diagonal, then the selector and contact rank-one terms row by row
+  parfor4(team, 6 * N, [&](int j) {
+    const int k = j / 6, r = j - 6 * k;
+    ws.HD[kDiag * k + r * (r + 1) / 2 + r] += S.sigma;
+  });
+  team.sync();
+  PARFOR(r, nf) {
+    const int k = P.m.fixed_node[r], c = P.m.fixed_dof[r];
+    ws.HD[kDiag * k + c * (c + 1) / 2 + c] += ws.rho[r] * ws.as[3 * r] * ws.as[3 * r];
+  }
+  team.sync();
+  PARFOR(t, 6 * (m - nf)) {
+    const int ct = t / 6, e = t - 6 * ct;  // 6 packed entries of the 3x3 block
+    const int rr = e < 1 ? 0 : (e < 3 ? 1 : 2), cc = e - rr * (rr + 1) / 2;
+    const int row = nf + ct, k = ws.cnode[ct];
+    ws.HD[kDiag * k + e] += ws.rho[row] * ws.as[3 * row + rr] * ws.as[3 * row + cc];
   }
   team.sync();
   PROF_T0(t_fac);
   int fbad = twisted_factor(team, N, ws.HD, ws.HU, ws.scr, ws.sh);
   PROF_ADD(ws, PF_FACTOR, t_fac);
   if (fbad >= 0) return ST_LINALG;
+  twisted_q(team, N, ws.HU, ws.Qg);
   // initial iterate (solver.py:287-289)
   PARFOR(j, n) ws.xs[j] = 0.0;
   PARFOR(r, m) {
@@ -732,7 +762,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     }
     team.sync();
     PROF_T0(t_ch);
-    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0, ws.sh, ws.sh);
+    twisted_solve_la(team, N, ws.HD, ws.HU, ws.Qg, ws.rhs, ws.tmp, ws.xt, ws.sh);
     team.sync();
     PROF_ADD(ws, PF_CHAIN, t_ch);
     PARFOR(r, m) {
