@@ -724,7 +724,6 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   int fbad = twisted_factor(team, N, ws.HD, ws.HU, ws.scr, ws.sh);
   PROF_ADD(ws, PF_FACTOR, t_fac);
   if (fbad >= 0) return ST_LINALG;
-  twisted_q(team, N, ws.HU, ws.Qg);
   // initial iterate (solver.py:287-289)
   PARFOR(j, n) ws.xs[j] = 0.0;
   PARFOR(r, m) {
@@ -762,7 +761,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     }
     team.sync();
     PROF_T0(t_ch);
-    twisted_solve_la(team, N, ws.HD, ws.HU, ws.Qg, ws.rhs, ws.tmp, ws.xt, ws.sh);
+    twisted_solve(team, N, ws.HD, ws.HU, ws.rhs, ws.tmp, ws.xt, 1, 0, ws.sh, ws.sh);
     team.sync();
     PROF_ADD(ws, PF_CHAIN, t_ch);
     PARFOR(r, m) {
