@@ -31,22 +31,27 @@ __global__ void k_model_setup(int N, const double* rest, double* rest_dir, doubl
   model_setup(team, N, rest, rest_dir, rest_len, rest_frames, offsets, qa, qb, bad);
 }
 
-// persistent solve; one warp = one scenario at a time.  With hot_stride > 0
-// each warp's hot arrays (factor, iterate, row state) live in its slice of
-// dynamic shared memory; otherwise everything is in the global slab.
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+// persistent solve; one CTA of kTeamWarps warps = one scenario at a time.
+// With hot_stride > 0 the team's hot arrays (factor, iterate, row state)
+// live in dynamic shared memory; otherwise everything is in the global slab.
+constexpr int kTeamWarps = 2;
+
+__global__ void __launch_bounds__(32 * kTeamWarps)
     k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride, long hot_stride) {
   extern __shared__ double smem[];
-  TeamWarp team{(int)(threadIdx.x & 31)};
-  const int wib = threadIdx.x >> 5;
-  const long wid = (long)blockIdx.x * (blockDim.x >> 5) + wib;
-  double* hot = hot_stride > 0 ? smem + wib * hot_stride : nullptr;
+  __shared__ double red[kTeamWarps];
+  __shared__ int ired[kTeamWarps + 1];
+  __shared__ int next;
+  TeamCta team{TeamWarp{(int)(threadIdx.x & 31)}, (int)(threadIdx.x >> 5), kTeamWarps, red, ired};
+  const long wid = blockIdx.x;
+  double* hot = hot_stride > 0 ? smem : nullptr;
   Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish);
   ws.prof = B.prof ? B.prof + wid * PF_COUNT : nullptr;
   while (true) {
-    int s = 0;
-    if (team.lane == 0) s = atomicAdd(B.work_counter, 1);
-    s = __shfl_sync(0xffffffffu, s, 0);
+    if (threadIdx.x == 0) next = atomicAdd(B.work_counter, 1);
+    __syncthreads();
+    const int s = next;
+    __syncthreads();
     if (s >= B.S) break;
     run_scenario(team, P, B, s, ws);
   }
@@ -310,15 +315,14 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const char* force_global = getenv("ACCFEM_GLOBAL_WORKSPACE");
+    h->solve_warps = kTeamWarps;
     if (hot * 8 <= max_smem && !(force_global && force_global[0] == '1')) {
       h->hot_stride = hot;
-      h->solve_warps = 1;
       cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(hot * 8));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32, hot * 8);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kTeamWarps, hot * 8);
     } else {
       h->hot_stride = 0;
-      h->solve_warps = kWarpsPerBlock;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kWarpsPerBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kTeamWarps, 0);
     }
     if (h->blocks_per_sm < 1) h->blocks_per_sm = 1;
   }
@@ -360,7 +364,7 @@ static long grid_blocks(accfem_handle* h, long S) {
   return std::max(1L, std::min(want, cap));
 }
 
-extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm * h->solve_warps : 0; }
+extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm : 0; }
 extern "C" long long accfem_workspace_bytes(accfem_handle* h) { return h ? (long long)h->ws.n * 8 : 0; }
 extern "C" int accfem_launches(accfem_handle* h) { return h ? h->launches : 0; }
 
@@ -377,9 +381,8 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   }
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  const long wpb = h->solve_warps;
-  long blocks = std::max(1L, std::min((io->S + wpb - 1) / wpb, (long)h->sms * h->blocks_per_sm));
-  if (int rc = ensure_ws(h, blocks * wpb, h->cmax)) return rc;
+  long blocks = std::max(1L, std::min((long)io->S, (long)h->sms * h->blocks_per_sm));
+  if (int rc = ensure_ws(h, blocks, h->cmax)) return rc;
   BatchDev B;
   memset(&B, 0, sizeof(B));
   B.S = io->S;
@@ -400,8 +403,8 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
   B.prof = h->prof;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
-  k_solve<<<(unsigned)blocks, 32 * (unsigned)wpb, (size_t)(h->hot_stride * 8 * wpb), st>>>(h->P, B, h->ws.p,
-                                                                                           h->ws_stride, h->hot_stride);
+  k_solve<<<(unsigned)blocks, 32 * kTeamWarps, (size_t)(h->hot_stride * 8), st>>>(h->P, B, h->ws.p, h->ws_stride,
+                                                                                   h->hot_stride);
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
   return 0;

@@ -830,6 +830,32 @@ DEV void twisted_solve_multi(const TeamWarp& team, int N, const double* __restri
   }
   __syncwarp();
 }
+// CTA teams: the block-tridiagonal recurrences are warp-cooperative; warp 0
+// runs them while the other warps of the team wait at the barrier.
+DEV int twisted_factor(const TeamCta& t, int N, double* D, double* U, double* scratch, bool sh = false) {
+  return t.on_warp0([&](const TeamWarp& w) { return twisted_factor(w, N, D, U, scratch, sh); });
+}
+DEV void twisted_solve(const TeamCta& t, int N, const double* D, const double* U, const double* rhs, double* tmp,
+                       double* out, int nrhs, long stride, bool sh = false, bool shv = false) {
+  t.on_warp0([&](const TeamWarp& w) {
+    twisted_solve(w, N, D, U, rhs, tmp, out, nrhs, stride, sh, shv);
+    return 0;
+  });
+}
+DEV void twisted_solve_multi(const TeamCta& t, int N, const double* D, const double* U, const double* rhs,
+                             double* tmp, double* out, int nrhs, long stride) {
+  t.on_warp0([&](const TeamWarp& w) {
+    twisted_solve_multi(w, N, D, U, rhs, tmp, out, nrhs, stride);
+    return 0;
+  });
+}
+DEV void twisted_solve_la(const TeamCta& t, int N, const double* D, const double* U, const double* Qg, double* rhs,
+                          double* tmp, double* out, bool sh) {
+  t.on_warp0([&](const TeamWarp& w) {
+    twisted_solve_la(w, N, D, U, Qg, rhs, tmp, out, sh);
+    return 0;
+  });
+}
 #endif
 
 // y = M x for a symmetric block-tridiagonal (D, U) matrix (full 6x6 diagonal

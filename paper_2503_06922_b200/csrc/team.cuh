@@ -96,6 +96,92 @@ struct TeamWarp {
 };
 #endif
 
+#if defined(__CUDACC__)
+// A team of `nw` warps of one CTA working on one scenario: PARFOR strides
+// all 32*nw threads, sync is the CTA barrier, reductions combine the warp
+// butterflies through a few words of shared memory (fixed order, so results
+// are deterministic).
+struct TeamCta {
+  TeamWarp w;
+  int warp, nw;
+  double* red;  // nw doubles of shared scratch
+  int* ired;    // nw + 1 ints of shared scratch
+  DEV int rank() const { return 32 * warp + w.lane; }
+  DEV int size() const { return 32 * nw; }
+  DEV void sync() const { __syncthreads(); }
+  DEV double max(double v) const {
+    v = w.max(v);
+    if (w.lane == 0) red[warp] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int i = 1; i < nw; ++i) r = fmax(r, red[i]);
+    __syncthreads();
+    return r;
+  }
+  DEV double min(double v) const {
+    v = w.min(v);
+    if (w.lane == 0) red[warp] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int i = 1; i < nw; ++i) r = fmin(r, red[i]);
+    __syncthreads();
+    return r;
+  }
+  DEV double sum(double v) const {
+    v = w.sum(v);
+    if (w.lane == 0) red[warp] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int i = 1; i < nw; ++i) r += red[i];
+    __syncthreads();
+    return r;
+  }
+  DEV int isum(int v) const {
+    v = w.isum(v);
+    if (w.lane == 0) ired[warp] = v;
+    __syncthreads();
+    int r = 0;
+    for (int i = 0; i < nw; ++i) r += ired[i];
+    __syncthreads();
+    return r;
+  }
+  DEV int imin(int v) const {
+    v = w.imin(v);
+    if (w.lane == 0) ired[warp] = v;
+    __syncthreads();
+    int r = ired[0];
+    for (int i = 1; i < nw; ++i) r = ::min(r, ired[i]);
+    __syncthreads();
+    return r;
+  }
+  DEV int any(bool p) const { return isum(w.any(p) ? 1 : 0) > 0; }
+  DEV int ballot_prefix(bool p, int* total) const {
+    unsigned b = __ballot_sync(0xffffffffu, p);
+    if (w.lane == 0) ired[warp] = __popc(b);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int i = 0; i < nw; ++i) {
+      if (i < warp) before += ired[i];
+      tot += ired[i];
+    }
+    __syncthreads();
+    *total = tot;
+    return before + __popc(b & ((1u << w.lane) - 1u));
+  }
+  // run a warp-cooperative routine on warp 0 only, everyone waits; returns its int result
+  template <class F>
+  DEV int on_warp0(F&& f) const {
+    int r = 0;
+    if (warp == 0) r = f(w);
+    if (rank() == 0) ired[nw] = r;
+    __syncthreads();
+    r = ired[nw];
+    __syncthreads();
+    return r;
+  }
+};
+#endif
+
 struct TeamSerial {
   DEV int rank() const { return 0; }
   DEV int size() const { return 1; }
