@@ -779,6 +779,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
       ws.y[r] = y + rh * (zr - zn);
       ws.z[r] = zn;
     }
+    team.sync();  // every row has read x~ before the x update overwrites it
     // x update fused with the next iteration's rhs = sigma x - g_s (xt aliases rhs)
     parfor4(team, n, [&](int j) {
       const double xn = al * ws.xt[j] + (1.0 - al) * ws.xs[j];
