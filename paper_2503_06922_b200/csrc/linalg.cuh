@@ -522,10 +522,119 @@ DEV void twisted_solve_impl(const TeamWarp& team, int N, const double* __restric
   __syncwarp();
 }
 
+// Odd N (equal halves, no predicates): one block per dependent step, with
+// z_i = Dinv_i v_i formed inside sweep 1 from the shuffled v_i the next step
+// fetches anyway (off the critical path), so no separate z pass is needed.
+template <bool SH, bool SHV>
+DEV void twisted_solve_odd(const TeamWarp& team, int N, const double* __restrict__ D, const double* __restrict__ U,
+                           const double* rhs, double* tmp, double* out) {
+  if (SH) {
+    __builtin_assume(__isShared(D));
+    __builtin_assume(__isShared(U));
+  }
+  if (SHV) {
+    __builtin_assume(__isShared(rhs));
+    __builtin_assume(__isShared(tmp));
+    __builtin_assume(__isShared(out));
+  }
+  const int lane = team.lane;
+  const int sub = lane < 6 ? 0 : (lane < 12 ? 1 : 2);  // lanes >= 12 shadow the top half
+  const int r = lane % 6;
+  const bool act = sub < 2;
+  const bool top = sub != 1;
+  const int base = top ? 0 : 6;
+  const int k = twist_split(N), K = k;
+  const int o0 = sidx(r, 0), o1 = sidx(r, 1), o2 = sidx(r, 2), o3 = sidx(r, 3), o4 = sidx(r, 4), o5 = sidx(r, 5);
+  (void)tmp;
+  // sweep 1: v at distance K..1 (top blocks 0..k-1, bottom N-1..k+1)
+  const int db = top ? 6 : -6, dM = top ? 36 : -36, dD = top ? kDiag : -kDiag;
+  const double* bp = rhs + (top ? 0 : 6 * (N - 1)) + r;
+  double* zp = out + (top ? 0 : 6 * (N - 1)) + r;
+  const double* Dp = D + (top ? 0 : kDiag * (N - 1));
+  const double* Mp = (top ? U : U + 36 * (N - 2)) + 6 * r;
+  double prev = *bp;
+  double p0, p1, p2, p3, p4, p5;
+  for (int t = 1; t < K; ++t) {
+    bp += db;
+    const double a0 = *bp;
+    const double m0 = Mp[0], m1 = Mp[1], m2 = Mp[2], m3 = Mp[3], m4 = Mp[4], m5 = Mp[5];
+    const double d0 = Dp[o0], d1 = Dp[o1], d2 = Dp[o2], d3 = Dp[o3], d4 = Dp[o4], d5 = Dp[o5];
+    Mp += dM;
+    p0 = __shfl_sync(0xffffffffu, prev, base + 0);
+    p1 = __shfl_sync(0xffffffffu, prev, base + 1);
+    p2 = __shfl_sync(0xffffffffu, prev, base + 2);
+    p3 = __shfl_sync(0xffffffffu, prev, base + 3);
+    p4 = __shfl_sync(0xffffffffu, prev, base + 4);
+    p5 = __shfl_sync(0xffffffffu, prev, base + 5);
+    prev = a0 - ((m0 * p0 + m2 * p2 + m4 * p4) + (m1 * p1 + m3 * p3 + m5 * p5));
+    // z of the block just left behind: Dinv row r times its v
+    const double z = (d0 * p0 + d2 * p2 + d4 * p4) + (d1 * p1 + d3 * p3 + d5 * p5);
+    if (act) *zp = z;
+    zp += db;
+    Dp += dD;
+  }
+  // middle: fetch v at distance 1 once more: z of that block and the coupling part
+  double part;
+  {
+    const double* M = (top ? U + 36 * (k > 0 ? k - 1 : 0) : U + 36 * k) + 6 * r;
+    const double m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5];
+    const double d0 = Dp[o0], d1 = Dp[o1], d2 = Dp[o2], d3 = Dp[o3], d4 = Dp[o4], d5 = Dp[o5];
+    p0 = __shfl_sync(0xffffffffu, prev, base + 0);
+    p1 = __shfl_sync(0xffffffffu, prev, base + 1);
+    p2 = __shfl_sync(0xffffffffu, prev, base + 2);
+    p3 = __shfl_sync(0xffffffffu, prev, base + 3);
+    p4 = __shfl_sync(0xffffffffu, prev, base + 4);
+    p5 = __shfl_sync(0xffffffffu, prev, base + 5);
+    part = K > 0 ? (m0 * p0 + m1 * p1 + m2 * p2 + m3 * p3 + m4 * p4 + m5 * p5) : 0.0;
+    const double z = (d0 * p0 + d2 * p2 + d4 * p4) + (d1 * p1 + d3 * p3 + d5 * p5);
+    if (act && K > 0) *zp = z;
+  }
+  const double opart = __shfl_sync(0xffffffffu, part, (top ? 6 : 0) + r);
+  const double tk = rhs[6 * k + r] - ((top ? part : opart) + (top ? opart : part));
+  double xk;
+  {
+    const double* Dk = D + kDiag * k;
+    const double d0 = Dk[o0], d1 = Dk[o1], d2 = Dk[o2], d3 = Dk[o3], d4 = Dk[o4], d5 = Dk[o5];
+    const double q0 = __shfl_sync(0xffffffffu, tk, base + 0), q1 = __shfl_sync(0xffffffffu, tk, base + 1);
+    const double q2 = __shfl_sync(0xffffffffu, tk, base + 2), q3 = __shfl_sync(0xffffffffu, tk, base + 3);
+    const double q4 = __shfl_sync(0xffffffffu, tk, base + 4), q5 = __shfl_sync(0xffffffffu, tk, base + 5);
+    xk = (d0 * q0 + d2 * q2 + d4 * q4) + (d1 * q1 + d3 * q3 + d5 * q5);
+  }
+  __syncwarp();  // z written; rhs fully consumed (out may alias rhs)
+  if (sub == 0) out[6 * k + r] = xk;
+  // sweep 2: x at distance 1..K: x = z - M2^T x_prev (column r of M2)
+  double xp = xk;
+  double* xo = out + 6 * k + r;
+  const int dx = top ? -6 : 6;
+  const double* Cp = (top ? U + 36 * (k > 0 ? k - 1 : 0) : U + 36 * k) + r;
+  const int dC = top ? -36 : 36;
+  for (int t = 0; t < K; ++t) {
+    xo += dx;
+    const double z = *xo;
+    const double m0 = Cp[0], m1 = Cp[6], m2 = Cp[12], m3 = Cp[18], m4 = Cp[24], m5 = Cp[30];
+    Cp += dC;
+    p0 = __shfl_sync(0xffffffffu, xp, base + 0);
+    p1 = __shfl_sync(0xffffffffu, xp, base + 1);
+    p2 = __shfl_sync(0xffffffffu, xp, base + 2);
+    p3 = __shfl_sync(0xffffffffu, xp, base + 3);
+    p4 = __shfl_sync(0xffffffffu, xp, base + 4);
+    p5 = __shfl_sync(0xffffffffu, xp, base + 5);
+    xp = z - ((m0 * p0 + m2 * p2 + m4 * p4) + (m1 * p1 + m3 * p3 + m5 * p5));
+    if (act) *xo = xp;
+  }
+  __syncwarp();
+}
+
 DEV void twisted_solve(const TeamWarp& team, int N, const double* D, const double* U, const double* rhs, double* tmp,
                        double* out, int nrhs, long stride, bool sh = false, bool shv = false) {
   (void)nrhs;
   (void)stride;
+  if (N & 1) {
+    if (sh && shv) twisted_solve_odd<true, true>(team, N, D, U, rhs, tmp, out);
+    else if (sh) twisted_solve_odd<true, false>(team, N, D, U, rhs, tmp, out);
+    else twisted_solve_odd<false, false>(team, N, D, U, rhs, tmp, out);
+    return;
+  }
   if (sh && shv) twisted_solve_impl<true, true>(team, N, D, U, rhs, tmp, out);
   else if (sh) twisted_solve_impl<true, false>(team, N, D, U, rhs, tmp, out);
   else twisted_solve_impl<false, false>(team, N, D, U, rhs, tmp, out);
