@@ -365,7 +365,7 @@ def main():
                          "frac": achieved / peak, "traffic": None,
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in "
                                         "MEASURED_PEAKS.json)",
-                         "flop_per_solve": fl, "kernel": "k_solve (persistent, one warp per scenario)"},
+                         "flop_per_solve": fl, "kernel": "k_solve (persistent, one 2-warp CTA per scenario, 3 CTAs/SM)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
             "latency": {"batch": 1, "wall_clock": "solve_static_batch + cudaDeviceSynchronize", **lat},
         }
