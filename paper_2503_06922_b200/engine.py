@@ -69,6 +69,15 @@ class BatchResult:
         return BatchResult(**out)
 
 
+@dataclass
+class BatchState:
+    """Per-scenario cross-frame solver state of the batched frame mode."""
+
+    warm_y: object       # (S, N) contact multipliers by node
+    warm_fixed: object   # (S, n_fixed) selector multipliers, or None before the first frame
+    rho: object          # (S,)
+
+
 class Engine:
     """Single-writer stepping loop over one robot/mesh/constraint setup."""
 
@@ -341,6 +350,61 @@ class Engine:
         self._check(rc)
         out._keep = keep  # inputs must outlive the asynchronous launch
         return out
+
+    # -- batched frame mode (real-time stepping) -------------
+    def initial_batch_state(self, S):
+        """Fresh cross-frame solver state for S scenarios (engine.py:100-103)."""
+        import torch
+        return BatchState(warm_y=torch.zeros((S, self.model.node_count), dtype=torch.float64, device=self.device),
+                          warm_fixed=None,
+                          rho=torch.full((S,), float(self.settings.rho), dtype=torch.float64, device=self.device))
+
+    def step_batch(self, x, tensions=None, applied=None, insertion=None, state=None, stream=None):
+        """One `Engine.step` (engine.py:136-240) for each of S scenarios.
+
+        x (S, 6N), tensions (S, n_cables), applied (S, 6N), insertion (S,) are
+        torch CUDA tensors; `state` carries each scenario's warm multipliers and
+        rho between frames (a fresh state if None).  Returns (BatchResult with
+        the new coords and last-frame contacts, per-frame stats (S, 12) in the
+        layout of include/accfem.h ACCFEM_TRACE_STATS, new BatchState).
+        """
+        import torch
+
+        S, N = int(x.shape[0]), self.model.node_count
+        nf = len(self._rows)
+        if state is None:
+            state = self.initial_batch_state(S)
+        out = self.allocate_batch(S)
+        stats = torch.zeros((S, 1, _lib.TRACE_STATS), dtype=torch.float64, device=self.device)
+        new = BatchState(warm_y=torch.zeros_like(state.warm_y),
+                         warm_fixed=torch.zeros((S, max(nf, 1)), dtype=torch.float64, device=self.device),
+                         rho=torch.zeros_like(state.rho))
+        keep = [t.contiguous() if t is not None else None for t in (x, tensions, applied, insertion)]
+        desc = _lib.BatchDesc()
+        desc.S = S
+        desc.x0 = _lib.ptr(keep[0])
+        desc.tensions = _lib.ptr(keep[1]) if self.cables else None
+        desc.applied = _lib.ptr(keep[2])
+        desc.insertion = _lib.ptr(keep[3])
+        desc.warm_y_in = _lib.ptr(state.warm_y)
+        desc.warm_fixed_in = _lib.ptr(state.warm_fixed)
+        desc.rho_in = _lib.ptr(state.rho)
+        for name in ("coords", "status", "frames", "converged", "residual", "n_contacts", "contact_node",
+                     "contact_triangle", "contact_gap", "contact_multiplier", "contact_force", "contact_normal",
+                     "contact_point"):
+            setattr(desc, name, _lib.ptr(getattr(out, name)))
+        desc.warm_y_out, desc.warm_fixed_out, desc.rho_out = (_lib.ptr(new.warm_y), _lib.ptr(new.warm_fixed),
+                                                              _lib.ptr(new.rho))
+        desc.trace_cap, desc.trace_stats = 1, _lib.ptr(stats)
+        desc.max_frames, desc.stop_on_tol, desc.tol, desc.fail_on_limit = 1, 0, 0.0, 0
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        self._check(self._lib.accfem_solve_batch(self._h, ctypes.byref(desc), ctypes.c_void_p(st.cuda_stream)))
+        out._keep = keep
+        if nf == 0:
+            new.warm_fixed = None
+        else:
+            new.warm_fixed = new.warm_fixed[:, :nf]
+        return out, stats[:, 0, :], new
 
     # -- unit entry points ---------------------------------------------------------
     def element_pass(self, x):

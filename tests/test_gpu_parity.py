@@ -217,3 +217,34 @@ def test_empty_batch_and_launch_count():
     before = eng.launches
     out = eng.solve_static_batch(torch.zeros((0, w.model.dof_count), dtype=torch.float64, device=DEV))
     assert eng.launches == before and out.coords.shape[0] == 0
+
+
+def test_step_batch_frame_mode_with_insertion_matches_oracle():
+    """Batched real-time frame mode (engine.py:300-316 semantics): 6 frames of
+    cfg3p with an insertion increment and a load ramp, 4 scenarios, against
+    the oracle's Engine.step with the same inputs (insertion via b_fn,
+    engine.py:123-134)."""
+    from paper_2503_06922_b200.engine import Engine
+    w = scenarios.cfg3p(4)
+    eng = Engine(**w.engine_kwargs(), device=0)
+    S = w.size
+    x = torch.tensor(w.x0, device=DEV)
+    ins = torch.tensor([0.0, 1e-4, 2e-4, 5e-4], device=DEV, dtype=torch.float64)
+    state = None
+    oracles = [O.OracleEngine(**w.engine_kwargs()) for _ in range(S)]
+    ox = [w.x0[i].copy() for i in range(S)]
+    for f in range(6):
+        scale = 0.5 + 0.1 * f
+        app = torch.tensor(w.applied * scale, device=DEV)
+        out, stats, state = eng.step_batch(x, None, app, ins, state)
+        torch.cuda.synchronize()
+        x = out.coords
+        r = out.to_numpy()
+        st = stats.cpu().numpy()
+        for i in range(S):
+            fr = oracles[i].step(ox[i], None, w.applied[i] * scale, insertion=float(ins[i]))
+            ox[i] = fr.coords
+            assert int(r.status[i]) == 0
+            assert int(st[i, 5]) == fr.iterations and int(st[i, 6]) == fr.n_c
+            assert np.abs(r.coords[i] - fr.coords).max() <= 1e-9 * np.abs(fr.coords).max()
+            assert abs(st[i, 0] - fr.dx_norm) <= 1e-6 * fr.dx_norm + 1e-12
