@@ -42,11 +42,14 @@ __global__ void __launch_bounds__(32 * kTeamWarps)
   __shared__ double red[kTeamWarps];
   __shared__ int ired[kTeamWarps + 1];
   __shared__ int next;
+  __shared__ unsigned long long prof_acc[PF_COUNT];  // phase counters accumulate in shared memory
   TeamCta team{TeamWarp{(int)(threadIdx.x & 31)}, (int)(threadIdx.x >> 5), kTeamWarps, red, ired};
   const long wid = blockIdx.x;
   double* hot = hot_stride > 0 ? smem : nullptr;
   Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish);
-  ws.prof = B.prof ? B.prof + wid * PF_COUNT : nullptr;
+  if (threadIdx.x < PF_COUNT) prof_acc[threadIdx.x] = 0;
+  ws.prof = B.prof ? prof_acc : nullptr;
+  __syncthreads();
   while (true) {
     if (threadIdx.x == 0) next = atomicAdd(B.work_counter, 1);
     __syncthreads();
@@ -55,6 +58,8 @@ __global__ void __launch_bounds__(32 * kTeamWarps)
     if (s >= B.S) break;
     run_scenario(team, P, B, s, ws);
   }
+  __syncthreads();
+  if (B.prof && threadIdx.x < PF_COUNT) B.prof[wid * PF_COUNT + threadIdx.x] = prof_acc[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
