@@ -15,14 +15,19 @@
 #include <vector>
 
 #include "../../include/accfem.h"
-#include "engine.cuh"
 #include "host_build.hpp"
+#include "ksolve.cuh"
 
 using namespace accfem;
 
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
+// k_solve team widths: throughput mode (three 2-warp teams per SM share it)
+// and latency mode (batches that leave SMs idle get 4-warp teams, whose
+// parallel phases run twice as wide; measured p50 -15% at batch 1)
+constexpr int kTeamWarps = 2;
+constexpr int kLatencyTeamWarps = 4;
 
 __global__ void k_model_setup(int N, const double* rest, double* rest_dir, double* rest_len, double* rest_frames,
                               double* offsets, double* qa, double* qb, int* bad) {
@@ -31,35 +36,13 @@ __global__ void k_model_setup(int N, const double* rest, double* rest_dir, doubl
   model_setup(team, N, rest, rest_dir, rest_len, rest_frames, offsets, qa, qb, bad);
 }
 
-// persistent solve; one CTA of kTeamWarps warps = one scenario at a time.
-// With hot_stride > 0 the team's hot arrays (factor, iterate, row state)
-// live in dynamic shared memory; otherwise everything is in the global slab.
-constexpr int kTeamWarps = 2;
-
-__global__ void __launch_bounds__(32 * kTeamWarps)
-    k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride, long hot_stride) {
-  extern __shared__ double smem[];
-  __shared__ double red[kTeamWarps];
-  __shared__ int ired[kTeamWarps + 1];
-  __shared__ int next;
-  __shared__ unsigned long long prof_acc[PF_COUNT];  // phase counters accumulate in shared memory
-  TeamCta team{TeamWarp{(int)(threadIdx.x & 31)}, (int)(threadIdx.x >> 5), kTeamWarps, red, ired};
-  const long wid = blockIdx.x;
-  double* hot = hot_stride > 0 ? smem : nullptr;
-  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish);
-  if (threadIdx.x < PF_COUNT) prof_acc[threadIdx.x] = 0;
-  ws.prof = B.prof ? prof_acc : nullptr;
-  __syncthreads();
-  while (true) {
-    if (threadIdx.x == 0) next = atomicAdd(B.work_counter, 1);
-    __syncthreads();
-    const int s = next;
-    __syncthreads();
-    if (s >= B.S) break;
-    run_scenario(team, P, B, s, ws);
-  }
-  __syncthreads();
-  if (B.prof && threadIdx.x < PF_COUNT) B.prof[wid * PF_COUNT + threadIdx.x] = prof_acc[threadIdx.x];
+// k_solve<NW> lives in ksolve.cuh, one translation unit per team width
+// (ksolve_<NW>.cu, compiled in parallel); this table reaches them.
+static const KSolveEntry* solve_entry(int nw) {
+  static const KSolveEntry table[] = {ksolve_entry_2(), ksolve_entry_4()};
+  for (const KSolveEntry& e : table)
+    if (e.nw == nw) return &e;
+  return nullptr;
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock)
@@ -145,8 +128,10 @@ struct DevBuf {
 struct accfem_handle {
   int device = 0;
   int sms = 0;
-  int blocks_per_sm = 0;     // k_solve occupancy in the chosen mode
-  int solve_warps = 0;       // warps per k_solve block
+  int blocks_per_sm = 0;     // k_solve occupancy, throughput mode
+  int solve_warps = 0;       // warps per k_solve block, throughput mode
+  int lat_blocks_per_sm = 0; // the same for latency mode
+  int lat_warps = 0;
   long hot_stride = 0;       // doubles of shared memory per warp (0: global mode)
   int launches = 0;
   std::string err;
@@ -313,23 +298,28 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
     delete h;
     return ACCFEM_E_DOMAIN;
   }
-  // launch mode: hot arrays in shared memory (one warp per block) when they fit
+  // launch mode: hot arrays in shared memory when they fit; team width from
+  // ACCFEM_TEAM_WARPS (development override) or the default
   {
     long hot = ws_hot_doubles(N, sd->n_fixed);
     hot = (hot + 15) & ~15L;
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const char* force_global = getenv("ACCFEM_GLOBAL_WORKSPACE");
+    const char* tw = getenv("ACCFEM_TEAM_WARPS");
     h->solve_warps = kTeamWarps;
-    if (hot * 8 <= max_smem && !(force_global && force_global[0] == '1')) {
-      h->hot_stride = hot;
-      cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(hot * 8));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kTeamWarps, hot * 8);
-    } else {
-      h->hot_stride = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, k_solve, 32 * kTeamWarps, 0);
+    h->lat_warps = kLatencyTeamWarps;
+    if (tw && solve_entry(atoi(tw))) h->solve_warps = h->lat_warps = atoi(tw);
+    const bool in_smem = hot * 8 <= max_smem && !(force_global && force_global[0] == '1');
+    h->hot_stride = in_smem ? hot : 0;
+    for (int mode = 0; mode < 2; ++mode) {
+      const int nw = mode ? h->lat_warps : h->solve_warps;
+      int* bps = mode ? &h->lat_blocks_per_sm : &h->blocks_per_sm;
+      const void* kern = solve_entry(nw)->kernel;
+      if (in_smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(hot * 8));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, 32 * nw, in_smem ? hot * 8 : 0);
+      if (*bps < 1) *bps = 1;
     }
-    if (h->blocks_per_sm < 1) h->blocks_per_sm = 1;
   }
   *out = h;
   return 0;
@@ -386,7 +376,10 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   }
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  long blocks = std::max(1L, std::min((long)io->S, (long)h->sms * h->blocks_per_sm));
+  // latency mode when the batch fits the wide teams' residency
+  const bool lat = (long)io->S <= (long)h->sms * h->lat_blocks_per_sm;
+  const int nw = lat ? h->lat_warps : h->solve_warps;
+  long blocks = std::max(1L, std::min((long)io->S, (long)h->sms * (lat ? h->lat_blocks_per_sm : h->blocks_per_sm)));
   if (int rc = ensure_ws(h, blocks, h->cmax)) return rc;
   BatchDev B;
   memset(&B, 0, sizeof(B));
@@ -408,8 +401,8 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
   B.prof = h->prof;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
-  k_solve<<<(unsigned)blocks, 32 * kTeamWarps, (size_t)(h->hot_stride * 8), st>>>(h->P, B, h->ws.p, h->ws_stride,
-                                                                                   h->hot_stride);
+  CUDA_OK(h, solve_entry(nw)->launch((unsigned)blocks, (size_t)(h->hot_stride * 8), st, h->P, B, h->ws.p,
+                                                  h->ws_stride, h->hot_stride));
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
   return 0;

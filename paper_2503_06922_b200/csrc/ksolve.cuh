@@ -1,0 +1,66 @@
+// The persistent solve kernel k_solve<NW> (one CTA of NW warps = one
+// scenario at a time) and its per-width launch entry points.  Each width is
+// instantiated in its own translation unit (ksolve_<NW>.cu) so the build
+// compiles them in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+
+namespace accfem {
+
+struct KSolveEntry {
+  int nw;
+  const void* kernel;  // for cudaFuncSetAttribute / occupancy queries
+  cudaError_t (*launch)(unsigned grid, size_t smem, cudaStream_t st, const Problem& P, const BatchDev& B,
+                        double* ws_base, long ws_stride, long hot_stride);
+};
+
+KSolveEntry ksolve_entry_2();
+KSolveEntry ksolve_entry_4();
+
+#if defined(ACCFEM_KSOLVE_NW)
+// persistent solve; one CTA of NW warps = one scenario at a time.
+// With hot_stride > 0 the team's hot arrays (factor, iterate, row state)
+// live in dynamic shared memory; otherwise everything is in the global slab.
+template <int NW>
+__global__ void __launch_bounds__(32 * NW)
+    k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride, long hot_stride) {
+  extern __shared__ double smem[];
+  __shared__ double red[NW];
+  __shared__ int ired[NW + 1];
+  __shared__ int next;
+  __shared__ unsigned long long prof_acc[PF_COUNT];  // phase counters accumulate in shared memory
+  TeamCta team{TeamWarp{(int)(threadIdx.x & 31)}, (int)(threadIdx.x >> 5), NW, red, ired};
+  const long wid = blockIdx.x;
+  double* hot = hot_stride > 0 ? smem : nullptr;
+  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish);
+  if (threadIdx.x < PF_COUNT) prof_acc[threadIdx.x] = 0;
+  ws.prof = B.prof ? prof_acc : nullptr;
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) next = atomicAdd(B.work_counter, 1);
+    __syncthreads();
+    const int s = next;
+    __syncthreads();
+    if (s >= B.S) break;
+    run_scenario(team, P, B, s, ws);
+  }
+  __syncthreads();
+  if (B.prof && threadIdx.x < PF_COUNT) B.prof[wid * PF_COUNT + threadIdx.x] = prof_acc[threadIdx.x];
+}
+
+template <int NW>
+static cudaError_t ksolve_launch(unsigned grid, size_t smem, cudaStream_t st, const Problem& P, const BatchDev& B,
+                                 double* ws_base, long ws_stride, long hot_stride) {
+  k_solve<NW><<<grid, 32 * NW, smem, st>>>(P, B, ws_base, ws_stride, hot_stride);
+  return cudaGetLastError();
+}
+#define ACCFEM_KSOLVE_PASTE2(a, b) a##b
+#define ACCFEM_KSOLVE_PASTE(a, b) ACCFEM_KSOLVE_PASTE2(a, b)
+KSolveEntry ACCFEM_KSOLVE_PASTE(ksolve_entry_, ACCFEM_KSOLVE_NW)() {
+  return KSolveEntry{ACCFEM_KSOLVE_NW, (const void*)k_solve<ACCFEM_KSOLVE_NW>, ksolve_launch<ACCFEM_KSOLVE_NW>};
+}
+#endif
+
+}  // namespace accfem

@@ -4,7 +4,8 @@ import ctypes, sys, time
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2503_06922_b200 import _lib, build, scenarios
-so = build.build(profile=True)
+import os
+so = os.environ.get("ACCFEM_PROF_SO") or build.build(profile=True)
 _lib._LIB = _lib.bind(ctypes.CDLL(so))
 _lib._LIB.accfem_dev_set_profile.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 from paper_2503_06922_b200.engine import Engine
