@@ -988,21 +988,44 @@ DEV double bt_row(int N, const double* D, const double* U, const double* x, int 
   return acc;
 }
 
+// One block row per thread: the three 6x6 blocks are loaded as 16-byte
+// vectors (54 independent loads in flight from L2), each output row keeps
+// bt_row's summation order.
 template <class Team>
 DEV void block_matvec(const Team& team, int N, const double* D, const double* U, const double* x, double* y) {
-  const int n = 6 * N;
-  const int stride = team.size();
-  for (int j0 = team.rank(); j0 < n; j0 += 4 * stride) {
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    const int j1 = j0 + stride, j2 = j0 + 2 * stride, j3 = j0 + 3 * stride;
-    a0 = bt_row(N, D, U, x, j0);
-    if (j1 < n) a1 = bt_row(N, D, U, x, j1);
-    if (j2 < n) a2 = bt_row(N, D, U, x, j2);
-    if (j3 < n) a3 = bt_row(N, D, U, x, j3);
-    y[j0] = a0;
-    if (j1 < n) y[j1] = a1;
-    if (j2 < n) y[j2] = a2;
-    if (j3 < n) y[j3] = a3;
+  PARFOR(k, N) {
+    double xk[6], acc[6];
+    ld6(x + 6 * k, xk);
+    {
+      double Dk[36];
+      ld36(D + 36 * k, Dk);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const double* dr = Dk + 6 * r;
+        acc[r] = dr[0] * xk[0] + dr[1] * xk[1] + dr[2] * xk[2] + dr[3] * xk[3] + dr[4] * xk[4] + dr[5] * xk[5];
+      }
+    }
+    if (k + 1 < N) {
+      double Uk[36], xn[6];
+      ld36(U + 36 * k, Uk);
+      ld6(x + 6 * (k + 1), xn);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const double* ur = Uk + 6 * r;
+        acc[r] += ur[0] * xn[0] + ur[1] * xn[1] + ur[2] * xn[2] + ur[3] * xn[3] + ur[4] * xn[4] + ur[5] * xn[5];
+      }
+    }
+    if (k > 0) {
+      double Up[36], xp[6];
+      ld36(U + 36 * (k - 1), Up);
+      ld6(x + 6 * (k - 1), xp);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const double* up = Up + r;
+        acc[r] += up[0] * xp[0] + up[6] * xp[1] + up[12] * xp[2] + up[18] * xp[3] + up[24] * xp[4] + up[30] * xp[5];
+      }
+    }
+    st6(y + 6 * k, acc);
   }
   team.sync();
 }

@@ -68,6 +68,63 @@ DEV void directors_pass(const Team& team, const Problem& P, const double* x, Ws&
   team.sync();
 }
 
+// 3x3 block B_pq = F (K_local,pq F^T) of the rotated element matrix
+DEV void elem_block(const double* F, const double* kl, int p, int q, double* B) {
+  double T[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double* kr = kl + 12 * (3 * p + i) + 3 * q;
+      T[3 * i + j] = kr[0] * F[3 * j] + kr[1] * F[3 * j + 1] + kr[2] * F[3 * j + 2];
+    }
+  mat3_mul(F, T, B);
+}
+
+// symmetrised 6x6 diagonal part of node a (p0 = 0) or node b (p0 = 2):
+// 0.5 (X + X^T) of the blocks (p0..p0+1)^2, full 6x6 into out
+DEV void elem_sym_diag(const double* F, const double* kl, int p0, double* out) {
+  double B0[9], B1[9];
+  for (int h = 0; h < 2; ++h) {  // diagonal 3x3 blocks
+    elem_block(F, kl, p0 + h, p0 + h, B0);
+    double* o = out + 21 * h;  // (3h, 3h)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      o[6 * i + i] = B0[3 * i + i];
+#pragma unroll
+      for (int j = i + 1; j < 3; ++j) {
+        const double v = 0.5 * (B0[3 * i + j] + B0[3 * j + i]);
+        o[6 * i + j] = v;
+        o[6 * j + i] = v;
+      }
+    }
+  }
+  elem_block(F, kl, p0, p0 + 1, B0);
+  elem_block(F, kl, p0 + 1, p0, B1);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double v = 0.5 * (B0[3 * i + j] + B1[3 * j + i]);
+      out[6 * i + 3 + j] = v;
+      out[6 * (3 + j) + i] = v;
+    }
+}
+
+// coupling block (node a rows, node b columns): 0.5 (B_ab + B_ba^T)
+DEV void elem_coupling(const double* F, const double* kl, double* out) {
+  double B0[9], B1[9];
+  for (int al = 0; al < 2; ++al)
+    for (int be = 0; be < 2; ++be) {
+      elem_block(F, kl, al, 2 + be, B0);
+      elem_block(F, kl, 2 + be, al, B1);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) out[6 * (3 * al + i) + 3 * be + j] = 0.5 * (B0[3 * i + j] + B1[3 * j + i]);
+    }
+}
+
 // element frames, internal force and (optionally) the block-tridiagonal
 // tangent.  Returns 0, or the 1-based index of the first degenerate element
 // (beam.py:262-264).
@@ -115,42 +172,13 @@ DEV int element_pass(const Team& team, const Problem& P, const double* x, Ws& ws
     for (int b = 0; b < 4; ++b) mat3_vec(F, fl + 3 * b, ws.fe + 12 * e + 3 * b);
     if (tangent) {
       // 3x3 blocks B_pq = F kl_pq F^T of the element matrix, symmetrised
-      // (beam.py:341-346); stored as aa | bb | ab 6x6 blocks
-      double* ke = ws.ke + 108 * e;
-      for (int p = 0; p < 4; ++p) {
-        for (int q = 0; q < 4; ++q) {
-          double T[9], B[9];
-          for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) {
-              const double* kr = M.kl + 12 * (3 * p + i) + 3 * q;
-              T[3 * i + j] = kr[0] * F[3 * j] + kr[1] * F[3 * j + 1] + kr[2] * F[3 * j + 2];
-            }
-          mat3_mul(F, T, B);
-          // place B (block p,q) into the element 12x12: p,q in {0,1} node a, {2,3} node b
-          int na = p >> 1, nb = q >> 1;
-          int slot = (na == 0 && nb == 0) ? 0 : (na == 1 && nb == 1) ? 1 : (na == 0) ? 2 : 3;
-          int r0 = 3 * (p & 1), c0 = 3 * (q & 1);
-          for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) {
-              if (slot < 3) {
-                ke[36 * slot + 6 * (r0 + i) + (c0 + j)] = B[3 * i + j];
-              } else {
-                // block (b, a): fold its transpose into the ab slot for symmetrisation
-                double& t = ke[36 * 2 + 6 * (c0 + j) + (r0 + i)];
-                t = 0.5 * (t + B[3 * i + j]);
-              }
-            }
-        }
-      }
-      // symmetrise the diagonal slots: 0.5 (X + X^T)
-      for (int s = 0; s < 2; ++s)
-        for (int i = 0; i < 6; ++i)
-          for (int j = i + 1; j < 6; ++j) {
-            double a = ke[36 * s + 6 * i + j], b = ke[36 * s + 6 * j + i];
-            double v = 0.5 * (a + b);
-            ke[36 * s + 6 * i + j] = v;
-            ke[36 * s + 6 * j + i] = v;
-          }
+      // (beam.py:341-346), written straight into the block-tridiagonal
+      // storage: node a's diagonal part into KD[e], the coupling into KU[e];
+      // node b's diagonal part is added to KD[e+1] after the barrier below
+      elem_sym_diag(F, M.kl, 0, ws.KD + 36 * e);
+      elem_coupling(F, M.kl, ws.KU + 36 * e);
+      if (e == E - 1)
+        for (int i = 0; i < 36; ++i) ws.KD[36 * E + i] = 0.0;
     }
   }
   bad = team.imin(bad);
@@ -165,14 +193,14 @@ DEV int element_pass(const Team& team, const Problem& P, const double* x, Ws& ws
     ws.fint[i] = acc;
   }
   if (tangent) {
-    PARFOR(i, 36 * N) {
-      int k = i / 36, r = i % 36;
-      double acc = 0.0;
-      if (k > 0) acc += ws.ke[108 * (k - 1) + 36 + r];
-      if (k < E) acc += ws.ke[108 * k + r];
-      ws.KD[i] = acc;
+    // node b's part: KD[e+1] += sym(bb(e)) (recomputed from the stored frame;
+    // the sum equals the reference's bb + aa: addition commutes)
+    PARFOR(e, E) {
+      double bb[36];
+      elem_sym_diag(ws.frames + 9 * e, M.kl, 2, bb);
+      double* kd = ws.KD + 36 * (e + 1);
+      for (int i = 0; i < 36; ++i) kd[i] += bb[i];
     }
-    PARFOR(i, 36 * E) ws.KU[i] = ws.ke[108 * (i / 36) + 72 + (i % 36)];
   }
   team.sync();
   return 0;
