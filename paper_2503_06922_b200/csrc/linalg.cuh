@@ -30,7 +30,11 @@ DEV bool spd6_inv(const double* S, double* Inv) {
     for (int q = 0; q < j; ++q) a -= L[j * (j - 1) / 2 + q] * (L[j * (j - 1) / 2 + q] * d[q]);
     ok = ok && (a > 0.0);
     d[j] = a;
+#if defined(__CUDA_ARCH__)
+    di[j] = __drcp_rn(a);  // correctly rounded: the same bits as 1.0 / a, ~half the latency
+#else
     di[j] = 1.0 / a;
+#endif
 #pragma unroll
     for (int i = j + 1; i < 6; ++i) {
       double t = S[6 * i + j];

@@ -313,33 +313,52 @@ DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws)
     }
     const int cell = inside ? (c[2] * G.dims[1] + c[1]) * G.dims[0] + c[0] : 0;
     const int it0 = inside ? G.cell_start[cell] : 0, it1 = inside ? G.cell_start[cell + 1] : 0;
-    for (int it = it0; it < it1; ++it) {
-      const int t = G.cell_tris[it];
-      // exact reference AABB-vs-sphere leaf test (mesh.py:259-262)
-      double gg[3];
-      for (int a = 0; a < 3; ++a) {
-        double lo = G.lo[3 * t + a], hi = G.hi[3 * t + a];
-        double u = xsub(lo, p[a]), v = xsub(p[a], hi);
-        v = v > 0.0 ? v : 0.0;
-        gg[a] = u > v ? u : v;
+    // candidates in batches of four: the indices, then the AABBs of the
+    // batch are requested together (two L2 round trips per batch instead of
+    // two per candidate); the winner rule is order independent
+    for (int it = it0; it < it1; it += 4) {
+      int tb[4];
+      double lob[4][3], hib[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) tb[u] = it + u < it1 ? G.cell_tris[it + u] : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int tt = tb[u] >= 0 ? tb[u] : tb[0];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lob[u][a] = G.lo[3 * tt + a];
+          hib[u][a] = G.hi[3 * tt + a];
+        }
       }
-      if (!(edot3(gg, gg) <= r2)) continue;
-      const double* cor = G.corners + 9 * t;
-      double cl[3], off[3];
-      closest_point(p, cor, cor + 3, cor + 6, cl);
-      for (int a = 0; a < 3; ++a) off[a] = xsub(p[a], cl[a]);
-      double eu = enorm3(off);
-      double pg = edot3(G.normals + 3 * t, off);
-      double sg = pg >= 0.0 ? eu : -eu;
-      bool aligned = fabs(pg) >= xsub(xmul(0.9, eu), 1e-12);
-      if (!(sg <= margin && eu <= radius && aligned)) continue;
-      if (best_t < 0 || sg < best_s || (sg == best_s && t < best_t)) {
-        best_t = t;
-        best_s = sg;
-        best_gap = pg;
-        best_pp[0] = cl[0];
-        best_pp[1] = cl[1];
-        best_pp[2] = cl[2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = tb[u];
+        if (t < 0) continue;
+        // exact reference AABB-vs-sphere leaf test (mesh.py:259-262)
+        double gg[3];
+        for (int a = 0; a < 3; ++a) {
+          double uu = xsub(lob[u][a], p[a]), v = xsub(p[a], hib[u][a]);
+          v = v > 0.0 ? v : 0.0;
+          gg[a] = uu > v ? uu : v;
+        }
+        if (!(edot3(gg, gg) <= r2)) continue;
+        const double* cor = G.corners + 9 * t;
+        double cl[3], off[3];
+        closest_point(p, cor, cor + 3, cor + 6, cl);
+        for (int a = 0; a < 3; ++a) off[a] = xsub(p[a], cl[a]);
+        double eu = enorm3(off);
+        double pg = edot3(G.normals + 3 * t, off);
+        double sg = pg >= 0.0 ? eu : -eu;
+        bool aligned = fabs(pg) >= xsub(xmul(0.9, eu), 1e-12);
+        if (!(sg <= margin && eu <= radius && aligned)) continue;
+        if (best_t < 0 || sg < best_s || (sg == best_s && t < best_t)) {
+          best_t = t;
+          best_s = sg;
+          best_gap = pg;
+          best_pp[0] = cl[0];
+          best_pp[1] = cl[1];
+          best_pp[2] = cl[2];
+        }
       }
     }
     ws.ctri[k] = best_t;
