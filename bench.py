@@ -340,6 +340,15 @@ def main():
 
     line = None
     if rank == 0:
+        # DRAM bytes per launch of k_solve: dram__bytes_read + write per solve from the committed ncu
+        # --set full capture (profiles/k_solve_dram.json), times the scenarios of this launch
+        traffic, traffic_src = None, None
+        tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "k_solve_dram.json")
+        if os.path.exists(tf):
+            with open(tf) as fh:
+                td = json.load(fh)
+            traffic = td["dram_bytes_per_solve"] * B
+            traffic_src = td["source"]
         fl = flops_per_solve(eng, w)
         peak = fp64_peak_tflops(dev)
         achieved = fl * B / (ms * 1e-3) / 1e12
@@ -362,7 +371,7 @@ def main():
                        "status_counts": {str(k): int(v) for k, v in zip(*np.unique(status, return_counts=True))},
                        "mean_frames": float(frames.mean())},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in "
                                         "MEASURED_PEAKS.json)",
                          "flop_per_solve": fl, "kernel": "k_solve (persistent, one 2-warp CTA per scenario, 3 CTAs/SM)"},
