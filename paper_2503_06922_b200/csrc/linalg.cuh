@@ -293,6 +293,15 @@ DEV void twisted_solve_multi(const TeamSerial& t, int N, const double* D, const 
                              double* tmp, double* out, int nrhs, long stride) {
   twisted_solve(t, N, D, U, rhs, tmp, out, nrhs, stride);
 }
+// in-place solve of nrhs right-hand sides (rhs + g*stride) in chunks of
+// kMultiRhs; tmp holds kMultiRhs * stride doubles per warp of the team
+DEV void twisted_solve_chunks(const TeamSerial& t, int N, const double* D, const double* U, double* rhs, double* tmp,
+                              int nrhs, long stride) {
+  for (int c0 = 0; c0 < nrhs; c0 += kMultiRhs) {
+    const int nb = nrhs - c0 < kMultiRhs ? nrhs - c0 : kMultiRhs;
+    twisted_solve(t, N, D, U, rhs + (long)c0 * stride, tmp, rhs + (long)c0 * stride, nb, stride);
+  }
+}
 
 DEV int q_per_half(int N) {
   const int k = twist_split(N);
@@ -961,6 +970,16 @@ DEV void twisted_solve_multi(const TeamCta& t, int N, const double* D, const dou
     twisted_solve_multi(w, N, D, U, rhs, tmp, out, nrhs, stride);
     return 0;
   });
+}
+// every warp of the team solves its own chunks of kMultiRhs right-hand sides
+DEV void twisted_solve_chunks(const TeamCta& t, int N, const double* D, const double* U, double* rhs, double* tmp,
+                              int nrhs, long stride) {
+  for (int c0 = t.warp * kMultiRhs; c0 < nrhs; c0 += t.nw * kMultiRhs) {
+    const int nb = nrhs - c0 < kMultiRhs ? nrhs - c0 : kMultiRhs;
+    double* b = rhs + (long)c0 * stride;
+    twisted_solve_multi(t.w, N, D, U, b, tmp + (long)t.warp * kMultiRhs * stride, b, nb, stride);
+  }
+  t.sync();
 }
 DEV void twisted_solve_la(const TeamCta& t, int N, const double* D, const double* U, const double* Qg, double* rhs,
                           double* tmp, double* out, bool sh) {

@@ -523,23 +523,19 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
   if (reduced_factor(team, P, delta, ws) >= 0) return ST_OK;  // splu failure -> no polish
   PROF_ADD(ws, PF_POL_FACTOR, t_pf);
   PROF_T0(t_pw);
-  // W_c = P^{-1} C~_c, 16 contacts per warp pass (C~: contact row with selector DOFs zeroed)
-  for (int c0 = 0; c0 < nc; c0 += kMultiRhs) {
-    const int nb = nc - c0 < kMultiRhs ? nc - c0 : kMultiRhs;
-    double* Wb = ws.W + (long)c0 * n;
-    PARFOR(t, nb * n) Wb[t] = 0.0;
-    team.sync();
-    PARFOR(b, nb) {
-      const int c = c0 + b, nd = ws.cnode[c];
-      for (int a = 0; a < 3; ++a) {
-        const int j = 6 * nd + a;
-        if (P.m.fixed_row_of_dof[j] < 0) Wb[(long)b * n + j] = ws.cnrm[3 * c + a];
-      }
+  // W_c = P^{-1} C~_c (C~: contact row with selector DOFs zeroed); every warp
+  // of the team solves its own chunks of 16 contacts
+  parfor4(team, nc * n, [&](int t) { ws.W[t] = 0.0; });
+  team.sync();
+  PARFOR(c, nc) {
+    const int nd = ws.cnode[c];
+    for (int a = 0; a < 3; ++a) {
+      const int j = 6 * nd + a;
+      if (P.m.fixed_row_of_dof[j] < 0) ws.W[(long)c * n + j] = ws.cnrm[3 * c + a];
     }
-    team.sync();
-    twisted_solve_multi(team, N, ws.HD, ws.HU, Wb, ws.Wc, Wb, nb, n);
-    team.sync();
   }
+  team.sync();
+  twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, ws.Wc, nc, n);
   PARFOR(t, nc * nc) {
     const int p = t / nc, q = t - p * nc;
     const double* nr = ws.cnrm + 3 * p;

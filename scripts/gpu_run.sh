@@ -1,7 +1,8 @@
-# development run: GPU tests, throughput, latency, phase profile, op latencies
+# development run: GPU tests, throughput, latency, cfg5, phase profiles
 set -x
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python scripts/quick_tput.py 8192 3 > gpurun_out/tput.log 2>&1
 timeout 300 python scripts/latency.py > gpurun_out/lat.log 2>&1
+timeout 300 python scripts/cfg5_probe.py > gpurun_out/cfg5.log 2>&1
 ACCFEM_PROF_SO=paper_2503_06922_b200/libaccfem_prof.so timeout 300 python scripts/phase_profile.py cfg4 1776 > gpurun_out/prof.log 2>&1
-timeout 60 ./scripts/micro/op_lat > gpurun_out/op_lat.log 2>&1
+ACCFEM_PROF_SO=paper_2503_06922_b200/libaccfem_prof.so timeout 300 python scripts/phase_profile.py cfg5 148 > gpurun_out/prof5.log 2>&1

@@ -69,6 +69,24 @@ def test_static_solves_match_reference_goldens(golden, name):
         check_against_golden(g, f"{name}_{i}", r, i)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg4"])
+def test_global_workspace_mode_matches_reference_goldens(golden, name, monkeypatch):
+    """The global-workspace mode (hot set beyond shared memory, e.g. cfg5) forced on the
+    small configs: same results with every array in the per-team global slab."""
+    monkeypatch.setenv("ACCFEM_GLOBAL_WORKSPACE", "1")
+    g = golden("solves.npz")
+    if name == "cfg1":
+        w = scenarios.cfg1(3, seed=1)
+    elif name == "cfg4":
+        w = scenarios.cfg4(16)
+    else:
+        w = scenarios.CONFIGS[name](1)
+    r, eng = device_solve(w)
+    assert eng._lib.accfem_teams_resident(eng._h) > 0
+    for i in range(w.size):
+        check_against_golden(g, f"{name}_{i}", r, i)
+
+
 def test_cfg4_batch_matches_reference_goldens(golden):
     g = golden("solves.npz")
     w = scenarios.cfg4(16)
