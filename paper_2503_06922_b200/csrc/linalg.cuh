@@ -567,11 +567,28 @@ DEV void twisted_solve_odd(const TeamWarp& team, int N, const double* __restrict
   const double* Mp = (top ? U : U + 36 * (N - 2)) + 6 * r;
   double prev = *bp;
   double p0, p1, p2, p3, p4, p5;
+  // a factor in global memory (L2; the large-N mode) is software-pipelined:
+  // the rows of step t+1 are requested while step t computes
+  double nm0 = 0, nm1 = 0, nm2 = 0, nm3 = 0, nm4 = 0, nm5 = 0, nd0 = 0, nd1 = 0, nd2 = 0, nd3 = 0, nd4 = 0, nd5 = 0;
+  if (!SH && K > 1) {
+    nm0 = Mp[0]; nm1 = Mp[1]; nm2 = Mp[2]; nm3 = Mp[3]; nm4 = Mp[4]; nm5 = Mp[5];
+    nd0 = Dp[o0]; nd1 = Dp[o1]; nd2 = Dp[o2]; nd3 = Dp[o3]; nd4 = Dp[o4]; nd5 = Dp[o5];
+  }
   for (int t = 1; t < K; ++t) {
     bp += db;
     const double a0 = *bp;
-    const double m0 = Mp[0], m1 = Mp[1], m2 = Mp[2], m3 = Mp[3], m4 = Mp[4], m5 = Mp[5];
-    const double d0 = Dp[o0], d1 = Dp[o1], d2 = Dp[o2], d3 = Dp[o3], d4 = Dp[o4], d5 = Dp[o5];
+    double m0, m1, m2, m3, m4, m5, d0, d1, d2, d3, d4, d5;
+    if (!SH) {
+      m0 = nm0; m1 = nm1; m2 = nm2; m3 = nm3; m4 = nm4; m5 = nm5;
+      d0 = nd0; d1 = nd1; d2 = nd2; d3 = nd3; d4 = nd4; d5 = nd5;
+      const double* Mn = t + 1 < K ? Mp + dM : Mp;
+      const double* Dn = t + 1 < K ? Dp + dD : Dp;
+      nm0 = Mn[0]; nm1 = Mn[1]; nm2 = Mn[2]; nm3 = Mn[3]; nm4 = Mn[4]; nm5 = Mn[5];
+      nd0 = Dn[o0]; nd1 = Dn[o1]; nd2 = Dn[o2]; nd3 = Dn[o3]; nd4 = Dn[o4]; nd5 = Dn[o5];
+    } else {
+      m0 = Mp[0]; m1 = Mp[1]; m2 = Mp[2]; m3 = Mp[3]; m4 = Mp[4]; m5 = Mp[5];
+      d0 = Dp[o0]; d1 = Dp[o1]; d2 = Dp[o2]; d3 = Dp[o3]; d4 = Dp[o4]; d5 = Dp[o5];
+    }
     Mp += dM;
     p0 = __shfl_sync(0xffffffffu, prev, base + 0);
     p1 = __shfl_sync(0xffffffffu, prev, base + 1);
@@ -621,10 +638,21 @@ DEV void twisted_solve_odd(const TeamWarp& team, int N, const double* __restrict
   const int dx = top ? -6 : 6;
   const double* Cp = (top ? U + 36 * (k > 0 ? k - 1 : 0) : U + 36 * k) + r;
   const int dC = top ? -36 : 36;
+  double nc0 = 0, nc1 = 0, nc2 = 0, nc3 = 0, nc4 = 0, nc5 = 0;
+  if (!SH && K > 0) {
+    nc0 = Cp[0]; nc1 = Cp[6]; nc2 = Cp[12]; nc3 = Cp[18]; nc4 = Cp[24]; nc5 = Cp[30];
+  }
   for (int t = 0; t < K; ++t) {
     xo += dx;
     const double z = *xo;
-    const double m0 = Cp[0], m1 = Cp[6], m2 = Cp[12], m3 = Cp[18], m4 = Cp[24], m5 = Cp[30];
+    double m0, m1, m2, m3, m4, m5;
+    if (!SH) {
+      m0 = nc0; m1 = nc1; m2 = nc2; m3 = nc3; m4 = nc4; m5 = nc5;
+      const double* Cn = t + 1 < K ? Cp + dC : Cp;
+      nc0 = Cn[0]; nc1 = Cn[6]; nc2 = Cn[12]; nc3 = Cn[18]; nc4 = Cn[24]; nc5 = Cn[30];
+    } else {
+      m0 = Cp[0]; m1 = Cp[6]; m2 = Cp[12]; m3 = Cp[18]; m4 = Cp[24]; m5 = Cp[30];
+    }
     Cp += dC;
     p0 = __shfl_sync(0xffffffffu, xp, base + 0);
     p1 = __shfl_sync(0xffffffffu, xp, base + 1);
