@@ -464,6 +464,40 @@ DEV bool dense_chol(const Team& team, int na, double* S) {
   return true;
 }
 
+#if defined(__CUDACC__)
+// CTA version: the scaled column k is also copied to the contiguous `col`,
+// and the trailing lower triangle is updated one row per warp with the lanes
+// along the row (coalesced; the generic version walks rem^2 items with the
+// column strided through memory).  Same operations per entry.
+DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
+  for (int k = 0; k < na; ++k) {
+    double piv = S[k * na + k];
+    if (!(piv > 0.0)) return false;
+    double l = sqrt(piv);
+    team.sync();
+    PARFOR(i, na - k) {
+      const int r = k + i;
+      const double v = (r == k) ? l : S[r * na + k] / l;
+      S[r * na + k] = v;
+      col[r] = v;
+    }
+    team.sync();
+    for (int r = k + 1 + team.warp; r < na; r += team.nw) {
+      const double cr = col[r];
+      double* Sr = S + (long)r * na;
+      for (int cc = k + 1 + team.w.lane; cc <= r; cc += 32) Sr[cc] -= cr * col[cc];
+    }
+    team.sync();
+  }
+  return true;
+}
+#endif
+template <class Team>
+DEV bool dense_chol(const Team& team, int na, double* S, double* col) {
+  (void)col;
+  return dense_chol(team, na, S);
+}
+
 template <class Team>
 DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
   for (int k = 0; k < na; ++k) {
@@ -579,7 +613,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
       ws.S[t] = v + (p == q ? delta : 0.0);
     }
     team.sync();
-    if (na > 0 && !dense_chol(team, na, ws.S)) return ST_OK;
+    if (na > 0 && !dense_chol(team, na, ws.S, ws.Sy)) return ST_OK;  // Sy[0, cmax): column scratch
     // y = S_a^{-1} (C v - b_C);  dx = v - W_act y
     PARFOR(q, na) yact[q] = ws.Cv[ws.alist[q]] - ws.up[nf + ws.alist[q]];
     team.sync();
