@@ -26,7 +26,6 @@ KSolveEntry ksolve_entry_4();
 template <int NW>
 __global__ void __launch_bounds__(32 * NW)
     k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride, long hot_stride) {
-  static_assert(NW <= kMaxTeamWarps, "per-warp scratch (Ws::Wc) is sized for kMaxTeamWarps");
   extern __shared__ double smem[];
   __shared__ double red[NW];
   __shared__ int ired[NW + 1];

@@ -294,12 +294,15 @@ DEV void twisted_solve_multi(const TeamSerial& t, int N, const double* D, const 
   twisted_solve(t, N, D, U, rhs, tmp, out, nrhs, stride);
 }
 // in-place solve of nrhs right-hand sides (rhs + g*stride) in chunks of
-// kMultiRhs; tmp holds kMultiRhs * stride doubles per warp of the team
-DEV void twisted_solve_chunks(const TeamSerial& t, int N, const double* D, const double* U, double* rhs, double* tmp,
-                              int nrhs, long stride) {
+// kMultiRhs.  The multi-RHS sweeps need no scratch: sweep 1 overwrites each
+// block's right-hand side with its v (read first), the middle block's is
+// read before anything is written to it, z and x replace v in place.
+DEV void twisted_solve_chunks(const TeamSerial& t, int N, const double* D, const double* U, double* rhs, int nrhs,
+                              long stride) {
   for (int c0 = 0; c0 < nrhs; c0 += kMultiRhs) {
     const int nb = nrhs - c0 < kMultiRhs ? nrhs - c0 : kMultiRhs;
-    twisted_solve(t, N, D, U, rhs + (long)c0 * stride, tmp, rhs + (long)c0 * stride, nb, stride);
+    double* b = rhs + (long)c0 * stride;
+    twisted_solve(t, N, D, U, b, b, b, nb, stride);
   }
 }
 
@@ -999,13 +1002,13 @@ DEV void twisted_solve_multi(const TeamCta& t, int N, const double* D, const dou
     return 0;
   });
 }
-// every warp of the team solves its own chunks of kMultiRhs right-hand sides
-DEV void twisted_solve_chunks(const TeamCta& t, int N, const double* D, const double* U, double* rhs, double* tmp,
-                              int nrhs, long stride) {
+// every warp of the team solves its own chunks of kMultiRhs right-hand sides, in place
+DEV void twisted_solve_chunks(const TeamCta& t, int N, const double* D, const double* U, double* rhs, int nrhs,
+                              long stride) {
   for (int c0 = t.warp * kMultiRhs; c0 < nrhs; c0 += t.nw * kMultiRhs) {
     const int nb = nrhs - c0 < kMultiRhs ? nrhs - c0 : kMultiRhs;
     double* b = rhs + (long)c0 * stride;
-    twisted_solve_multi(t.w, N, D, U, b, tmp + (long)t.warp * kMultiRhs * stride, b, nb, stride);
+    twisted_solve_multi(t.w, N, D, U, b, b, b, nb, stride);
   }
   t.sync();
 }

@@ -80,14 +80,13 @@ struct Ws {
   // scaled system; HD/HU hold H_s, then M, then its twisted factor in place
   double *HD, *HU, *gs, *d, *colh, *xs, *xt, *rhs, *w, *v, *tmp;
   // solution / polish
-  double *dx, *dxp, *yp, *S, *Sy, *Wc, *wfix, *scr, *W, *Sf, *Cv, *Qg;
+  double *dx, *dxp, *yp, *S, *Sy, *wfix, *scr, *W, *Sf, *Cv, *Qg;
   int *act, *alist;
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
   bool sh;                   // hot arrays live in shared memory
 };
 
-constexpr int kMultiRhs = 16;     // right-hand sides solved concurrently by one warp (2 lanes each)
-constexpr int kMaxTeamWarps = 4;  // widest k_solve team
+constexpr int kMultiRhs = 16;  // right-hand sides solved concurrently by one warp (2 lanes each)
 
 // Carve a team's workspace.  Arrays touched by every ADMM iteration (the
 // factor, the scaled iterate and the row state) come from `hot` (shared
@@ -120,7 +119,6 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   w.lo = take(m); w.up = take(m); w.e = take(m); w.yfull = take(m); w.warm = take(N);
   w.d = take(n); w.colh = take(n); w.w = take(n); w.v = take(n);
   w.dx = take(n); w.dxp = take(n); w.yp = take(m); w.S = take(cp * cp); w.Sy = take(3 * cp);
-  w.Wc = take(kMaxTeamWarps * kMultiRhs * n);  // multi-RHS sweep scratch, one chunk per warp
   w.W = take(cp * n);      // polish: P^{-1} C~_c for every contact c
   w.Sf = take(cp * cp);    // polish: C P^{-1} C~^T over all contacts
   w.Cv = take(cp);

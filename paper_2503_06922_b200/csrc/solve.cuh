@@ -569,7 +569,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     }
   }
   team.sync();
-  twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, ws.Wc, nc, n);
+  twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, nc, n);
   PARFOR(t, nc * nc) {
     const int p = t / nc, q = t - p * nc;
     const double* nr = ws.cnrm + 3 * p;
