@@ -156,6 +156,12 @@ int accfem_teams_resident(accfem_handle* h);
 long long accfem_workspace_bytes(accfem_handle* h);
 int accfem_launches(accfem_handle* h); /* kernels launched by this handle so far */
 
+/* broad-phase grid built on the device by accfem_create (replaces the
+ * AabbTree build, mesh.py:204-243): dims[3], cell count, list entries; and a
+ * copy of its CSR lists (cell_start[n_cells + 1], cell_tris[n_entries]) */
+int accfem_grid_shape(const accfem_handle* h, int32_t* dims, int64_t* n_cells, int64_t* n_entries);
+int accfem_grid_download(accfem_handle* h, int32_t* cell_start, int32_t* cell_tris);
+
 #ifdef __cplusplus
 }
 #endif

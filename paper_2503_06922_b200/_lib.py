@@ -77,6 +77,8 @@ SIGNATURES = {
     "accfem_teams_resident": (ctypes.c_int, [c_void_p]),
     "accfem_workspace_bytes": (ctypes.c_longlong, [c_void_p]),
     "accfem_launches": (ctypes.c_int, [c_void_p]),
+    "accfem_grid_shape": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "accfem_grid_download": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
 }
 
 _LIB = None

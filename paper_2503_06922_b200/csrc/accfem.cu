@@ -7,6 +7,8 @@
 //                     assembly, Ruiz, block Cholesky, ADMM, polish, update
 //   k_element_pass    unit entry point: F_int + block-tridiagonal K
 //   k_detect          unit entry point: per-node contact winner
+//   k_grid_*          broad-phase grid build over the lumen mesh (grid.cuh)
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,6 +17,7 @@
 #include <vector>
 
 #include "../../include/accfem.h"
+#include "grid.cuh"
 #include "host_build.hpp"
 #include "ksolve.cuh"
 
@@ -141,6 +144,8 @@ struct accfem_handle {
   DevBuf<int> fixed_node, fixed_dof, fixed_row_of_dof, bad;
   DevBuf<double> corners, normals, lo, hi;
   DevBuf<int> cell_start, cell_tris;
+  long grid_cells = 0, grid_entries = 0;
+  int grid_dims[3] = {0, 0, 0};
   DevBuf<double> ws;
   DevBuf<int> counter;
   long ws_stride = 0;
@@ -179,6 +184,55 @@ extern "C" int accfem_version(void) { return 1; }
 
 extern "C" const char* accfem_last_error(const accfem_handle* h) {
   return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+// cell lists of the broad-phase grid on the device (grid.cuh); the host has
+// sized the grid (hm.dims/h/rr) and uploaded the triangle AABBs
+static cudaError_t build_grid(accfem_handle* h, const accfem_host::HostMesh& hm) {
+  GridBuild g;
+  g.lo = h->lo.p;
+  g.hi = h->hi.p;
+  g.T = hm.T;
+  for (int a = 0; a < 3; ++a) {
+    g.dims[a] = hm.dims[a];
+    g.origin[a] = hm.origin[a];
+    h->grid_dims[a] = hm.dims[a];
+  }
+  g.h = hm.h;
+  g.inv_h = hm.inv_h;
+  g.rr = hm.rr;
+  const long ncell = hm.ncell;
+  h->grid_cells = ncell;
+  cudaError_t e;
+  DevBuf<int> count;
+  if ((e = count.alloc(ncell + 1)) != cudaSuccess) return e;
+  if ((e = h->cell_start.alloc(ncell + 1)) != cudaSuccess) return e;
+  cudaMemset(count.p, 0, (ncell + 1) * sizeof(int));
+  const int tb = 128, tblocks = (int)std::min<long>((hm.T + tb - 1) / tb, 148L * 16);
+  k_grid_count<<<tblocks, tb>>>(g, count.p);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1));
+  DevBuf<char> tmp;
+  if ((e = tmp.alloc(tmp_bytes)) != cudaSuccess) return e;
+  cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1));
+  int entries = 0;
+  if ((e = cudaMemcpy(&entries, h->cell_start.p + ncell, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return e;
+  h->grid_entries = entries;
+  if ((e = h->cell_tris.alloc(std::max(entries, 1))) != cudaSuccess) return e;
+  DevBuf<int> unsorted;
+  if ((e = unsorted.alloc(std::max(entries, 1))) != cudaSuccess) return e;
+  cudaMemcpy(count.p, h->cell_start.p, (ncell + 1) * sizeof(int), cudaMemcpyDeviceToDevice);
+  k_grid_fill<<<tblocks, tb>>>(g, count.p, unsorted.p);
+  k_grid_sort<<<(int)std::min<long>((ncell + 7) / 8, 148L * 64), 256>>>(ncell, h->cell_start.p, unsorted.p,
+                                                                      h->cell_tris.p);
+  h->launches += 3;
+  e = cudaDeviceSynchronize();
+  tmp.release();
+  count.release();
+  unsorted.release();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
 }
 
 extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc* mesh, const accfem_settings* sd,
@@ -249,7 +303,7 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
   }
   // mesh + grid
   accfem_host::HostMesh hm;
-  std::string merr = accfem_host::build_mesh(mesh, S.radius, hm);
+  std::string merr = accfem_host::build_mesh(mesh, S.radius, hm, /*with_lists=*/false);
   if (!merr.empty()) {
     g_create_error = merr;
     delete h;
@@ -260,8 +314,7 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
     UP(normals, hm.normals.data(), hm.normals.size());
     UP(lo, hm.lo.data(), hm.lo.size());
     UP(hi, hm.hi.data(), hm.hi.size());
-    UP(cell_start, hm.cell_start.data(), hm.cell_start.size());
-    UP(cell_tris, hm.cell_tris.data(), hm.cell_tris.size());
+    if (!rc && (e = build_grid(h, hm)) != cudaSuccess) rc = 1;
   }
 #undef UP
   if (rc || h->counter.alloc(4) != cudaSuccess) {
@@ -357,6 +410,24 @@ static long grid_blocks(accfem_handle* h, long S) {
   long want = (S + kWarpsPerBlock - 1) / kWarpsPerBlock;
   long cap = (long)h->sms * h->blocks_per_sm;
   return std::max(1L, std::min(want, cap));
+}
+
+extern "C" int accfem_grid_shape(const accfem_handle* h, int32_t* dims, int64_t* n_cells, int64_t* n_entries) {
+  if (!h || !dims || !n_cells || !n_entries) return ACCFEM_E_ARG;
+  for (int a = 0; a < 3; ++a) dims[a] = h->grid_dims[a];
+  *n_cells = h->grid_cells;
+  *n_entries = h->grid_entries;
+  return 0;
+}
+
+extern "C" int accfem_grid_download(accfem_handle* h, int32_t* cell_start, int32_t* cell_tris) {
+  if (!h || !cell_start || !cell_tris) return ACCFEM_E_ARG;
+  if (h->grid_cells == 0) return 0;
+  cudaSetDevice(h->device);
+  CUDA_OK(h, cudaMemcpy(cell_start, h->cell_start.p, (h->grid_cells + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+  if (h->grid_entries)
+    CUDA_OK(h, cudaMemcpy(cell_tris, h->cell_tris.p, h->grid_entries * sizeof(int), cudaMemcpyDeviceToHost));
+  return 0;
 }
 
 extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm : 0; }

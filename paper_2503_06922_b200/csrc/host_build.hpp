@@ -26,6 +26,9 @@ struct HostMesh {
   double origin[3] = {0, 0, 0};
   double inv_h = 1.0;
   int dims[3] = {1, 1, 1};
+  // grid construction parameters (shared bit-for-bit with the device build, grid.cuh)
+  double h = 1.0, rr = 0.0;
+  long ncell = 0;
 };
 
 inline int grid_cell_host(double x, double o, double inv_h, int dim) {
@@ -35,8 +38,9 @@ inline int grid_cell_host(double x, double o, double inv_h, int dim) {
   return (int)f;
 }
 
-// returns "" on success, else an error message
-inline std::string build_mesh(const accfem_mesh_desc* d, double radius, HostMesh& M) {
+// returns "" on success, else an error message.  with_lists = false stops after
+// the grid sizing (the device library builds the cell lists itself, grid.cuh)
+inline std::string build_mesh(const accfem_mesh_desc* d, double radius, HostMesh& M, bool with_lists = true) {
   M = HostMesh();
   if (!d || d->triangle_count <= 0) return "";
   const int T = d->triangle_count, V = d->vertex_count;
@@ -116,6 +120,10 @@ inline std::string build_mesh(const accfem_mesh_desc* d, double radius, HostMesh
   }
   for (int a = 0; a < 3; ++a) M.origin[a] = glo[a];
   M.inv_h = 1.0 / h;
+  M.h = h;
+  M.rr = rr;
+  M.ncell = ncell;
+  if (!with_lists) return "";
   // box distance between cell c (padded by 1e-6 h) and the AABB of triangle t
   auto near = [&](int t, const int* c) {
     double d2 = 0.0;

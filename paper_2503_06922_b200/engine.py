@@ -143,6 +143,18 @@ class Engine:
     def launches(self):
         return int(self._lib.accfem_launches(self._h))
 
+    def broad_phase_grid(self):
+        """The device-built broad-phase grid (the AabbTree's replacement,
+        mesh.py:204-243): (dims[3], cell_start[n_cells + 1], cell_tris)."""
+        dims = np.zeros(3, np.int32)
+        nc, ne = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._lib.accfem_grid_shape(self._h, dims.ctypes.data, ctypes.addressof(nc),
+                                                ctypes.addressof(ne)))
+        start = np.zeros(nc.value + 1, np.int32)
+        tris = np.zeros(max(ne.value, 1), np.int32)
+        self._check(self._lib.accfem_grid_download(self._h, start.ctypes.data, tris.ctypes.data))
+        return dims, start, tris[:ne.value]
+
     def initial_configuration(self):
         return Configuration(self.model.rest_configuration.copy(), timestep_index=0)
 

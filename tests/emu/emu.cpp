@@ -91,6 +91,21 @@ extern "C" EmuHandle* emu_create(const accfem_model_desc* md, const accfem_mesh_
 
 extern "C" void emu_destroy(EmuHandle* h) { delete h; }
 
+// the host grid build (checker for the device build, accfem_grid_download)
+extern "C" int emu_grid_shape(EmuHandle* h, int32_t* dims, int64_t* n_cells, int64_t* n_entries) {
+  for (int a = 0; a < 3; ++a) dims[a] = h->mesh.T ? h->mesh.dims[a] : 0;
+  *n_cells = h->mesh.T ? h->mesh.ncell : 0;
+  *n_entries = h->mesh.T ? h->mesh.cell_start.back() : 0;
+  return 0;
+}
+
+extern "C" int emu_grid_download(EmuHandle* h, int32_t* cell_start, int32_t* cell_tris) {
+  if (!h->mesh.T) return 0;
+  memcpy(cell_start, h->mesh.cell_start.data(), h->mesh.cell_start.size() * sizeof(int32_t));
+  memcpy(cell_tris, h->mesh.cell_tris.data(), h->mesh.cell_start.back() * sizeof(int32_t));
+  return 0;
+}
+
 extern "C" int emu_element_pass(EmuHandle* h, int S, const double* x, double* fint, double* kd, double* ku, int* bad) {
   const int N = h->N, n = 6 * N, E = N - 1;
   Ws ws = ws_carve(h->ws.data(), nullptr, N, h->n_fixed, h->cmax);

@@ -45,6 +45,8 @@ def lib():
         L.emu_solve_batch.argtypes = [ctypes.c_void_p, ctypes.POINTER(_lib.BatchDesc)]
         L.emu_element_pass.argtypes = [ctypes.c_void_p, ctypes.c_int] + [ctypes.c_void_p] * 5
         L.emu_detect.argtypes = [ctypes.c_void_p, ctypes.c_int] + [ctypes.c_void_p] * 4
+        L.emu_grid_shape.argtypes = [ctypes.c_void_p] * 4
+        L.emu_grid_download.argtypes = [ctypes.c_void_p] * 3
         _EMU = L
     return _EMU
 
@@ -76,6 +78,16 @@ class EmuEngine:
         self.L.emu_element_pass(self.h, S, x.ctypes.data, f.ctypes.data, kd.ctypes.data, ku.ctypes.data,
                                 bad.ctypes.data)
         return f, kd, ku, bad
+
+    def broad_phase_grid(self):
+        """Host build of the broad-phase grid (checker for Engine.broad_phase_grid)."""
+        dims = np.zeros(3, np.int32)
+        nc, ne = ctypes.c_int64(), ctypes.c_int64()
+        self.L.emu_grid_shape(self.h, dims.ctypes.data, ctypes.addressof(nc), ctypes.addressof(ne))
+        start = np.zeros(nc.value + 1, np.int32)
+        tris = np.zeros(max(ne.value, 1), np.int32)
+        self.L.emu_grid_download(self.h, start.ctypes.data, tris.ctypes.data)
+        return dims, start, tris[:ne.value]
 
     def detect(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
