@@ -208,7 +208,7 @@ static cudaError_t build_grid(accfem_handle* h, const accfem_host::HostMesh& hm)
   if ((e = count.alloc(ncell + 1)) != cudaSuccess) return e;
   if ((e = h->cell_start.alloc(ncell + 1)) != cudaSuccess) return e;
   cudaMemset(count.p, 0, (ncell + 1) * sizeof(int));
-  const int tb = 128, tblocks = (int)std::min<long>((hm.T + tb - 1) / tb, 148L * 16);
+  const int tb = 128, tblocks = (int)std::min<long>((hm.T + 3) / 4, 148L * 16);  // 4 warps, 1 triangle each
   k_grid_count<<<tblocks, tb>>>(g, count.p);
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1));

@@ -6,10 +6,10 @@
 // -- O(T x cells per triangle), the part that grows with 10^4-10^5 triangle
 // STL meshes -- are built here in four passes:
 //
-//   k_grid_count   one thread per triangle: count the cells within the query
+//   k_grid_count   one warp per triangle: count the cells within the query
 //                  radius of its AABB (atomicAdd per cell)
 //   scan           exclusive sum of the counts -> CSR cell_start
-//   k_grid_fill    one thread per triangle: claim a slot per cell
+//   k_grid_fill    one warp per triangle: claim a slot per cell
 //   k_grid_sort    one warp per cell: order its list by triangle id
 //
 // The result equals the host build (host_build.hpp) entry for entry: the
@@ -62,9 +62,12 @@ __device__ __forceinline__ bool grid_near(const GridBuild& g, const double* lo, 
   return d2 <= __dmul_rn(g.rr, g.rr);
 }
 
-// visit every cell within rr of triangle t's AABB, x fastest (host order)
+// visit every cell within rr of triangle t's AABB; the lanes of a warp split
+// the flattened (x fastest) cell range of the triangle, so a triangle spanning
+// many cells is not walked by one thread (the visit order does not matter:
+// count and fill only claim slots, k_grid_sort restores the host order)
 template <class F>
-__device__ __forceinline__ void grid_cells_of(const GridBuild& g, int t, F&& fn) {
+__device__ __forceinline__ void grid_cells_of(const GridBuild& g, int t, int lane, F&& fn) {
   int c0[3], c1[3];
   grid_tri_range(g, t, c0, c1);
   double lo[3], hi[3];
@@ -73,21 +76,30 @@ __device__ __forceinline__ void grid_cells_of(const GridBuild& g, int t, F&& fn)
     lo[a] = g.lo[3L * t + a];
     hi[a] = g.hi[3L * t + a];
   }
-  int c[3];
-  for (c[2] = c0[2]; c[2] <= c1[2]; ++c[2])
-    for (c[1] = c0[1]; c[1] <= c1[1]; ++c[1])
-      for (c[0] = c0[0]; c[0] <= c1[0]; ++c[0])
-        if (grid_near(g, lo, hi, c)) fn(((long)c[2] * g.dims[1] + c[1]) * g.dims[0] + c[0]);
+  const int nx = c1[0] - c0[0] + 1, ny = c1[1] - c0[1] + 1, nz = c1[2] - c0[2] + 1;
+  const long n = (long)nx * ny * nz;
+  for (long k = lane; k < n; k += 32) {
+    int c[3];
+    c[0] = c0[0] + (int)(k % nx);
+    c[1] = c0[1] + (int)((k / nx) % ny);
+    c[2] = c0[2] + (int)(k / ((long)nx * ny));
+    if (grid_near(g, lo, hi, c)) fn(((long)c[2] * g.dims[1] + c[1]) * g.dims[0] + c[0]);
+  }
 }
 
+// one warp per triangle
 __global__ void k_grid_count(GridBuild g, int* count) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < g.T; t += gridDim.x * blockDim.x)
-    grid_cells_of(g, t, [&](long c) { atomicAdd(count + c, 1); });
+  const int lane = threadIdx.x & 31;
+  const long warps = (long)gridDim.x * (blockDim.x >> 5);
+  for (long t = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.T; t += warps)
+    grid_cells_of(g, (int)t, lane, [&](long c) { atomicAdd(count + c, 1); });
 }
 
 __global__ void k_grid_fill(GridBuild g, int* fill, int* cell_tris) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < g.T; t += gridDim.x * blockDim.x)
-    grid_cells_of(g, t, [&](long c) { cell_tris[atomicAdd(fill + c, 1)] = t; });
+  const int lane = threadIdx.x & 31;
+  const long warps = (long)gridDim.x * (blockDim.x >> 5);
+  for (long t = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < g.T; t += warps)
+    grid_cells_of(g, (int)t, lane, [&](long c) { cell_tris[atomicAdd(fill + c, 1)] = (int)t; });
 }
 
 // one warp per cell: rank sort of the cell's (distinct) triangle ids from the
