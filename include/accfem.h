@@ -22,6 +22,10 @@
  * accfem_batch are DEVICE pointers unless passed to accfem_solve_batch_host,
  * which takes HOST pointers and performs the copies itself (timed e2e path).
  * A handle is bound to one device; calls on one handle are not thread-safe.
+ * Calls on one handle are ordered even across streams: a launch on a stream
+ * other than the previous call's waits for that call to finish (the handle's
+ * work queue and workspace are shared), and the caller's stream sees the
+ * results in stream order.
  * Return value: 0 on success, >= 100 on API/CUDA failure (message via
  * accfem_last_error); per-scenario outcomes are status codes below.
  */
@@ -88,7 +92,14 @@ typedef struct {
   double margin;                  /* Engine(margin=) */
   double eps_abs, eps_rel, rho, sigma, alpha, beta0;
   int32_t max_iterations, check_interval, adaptive_rho, scaling_iterations, polish;
-  int32_t polish_capacity;        /* max active contacts in a polish round (0: min(N, 256)) */
+  int32_t polish_capacity;        /* max contacts a polish can hold (0: min(N, 256)); a frame with more
+                                     contacts than this reports ACCFEM_CAPACITY */
+  /* capacities fixed at create: every device buffer a solve call uses is
+     allocated by accfem_create, so solve calls never allocate */
+  int32_t max_batch;              /* host-path staging, scenarios per chunk (0: 16384); larger host
+                                     batches are processed in chunks */
+  int32_t trace_slots;            /* host-path per-frame coords/contact trace staging, in
+                                     scenario-frames (0: 1024) */
 } accfem_settings;
 
 typedef struct {
@@ -155,6 +166,7 @@ int accfem_detect(accfem_handle* h, int32_t S, const double* x, int32_t* tri, do
 int accfem_teams_resident(accfem_handle* h);
 long long accfem_workspace_bytes(accfem_handle* h);
 int accfem_launches(accfem_handle* h); /* kernels launched by this handle so far */
+int accfem_max_batch(accfem_handle* h); /* host-path chunk size (accfem_settings.max_batch) */
 
 /* broad-phase grid built on the device by accfem_create (replaces the
  * AabbTree build, mesh.py:204-243): dims[3], cell count, list entries; and a

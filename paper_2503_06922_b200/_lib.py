@@ -39,7 +39,8 @@ class SettingsDesc(ctypes.Structure):
                 ("margin", c_double), ("eps_abs", c_double), ("eps_rel", c_double), ("rho", c_double),
                 ("sigma", c_double), ("alpha", c_double), ("beta0", c_double), ("max_iterations", c_int32),
                 ("check_interval", c_int32), ("adaptive_rho", c_int32), ("scaling_iterations", c_int32),
-                ("polish", c_int32), ("polish_capacity", c_int32)]
+                ("polish", c_int32), ("polish_capacity", c_int32), ("max_batch", c_int32),
+                ("trace_slots", c_int32)]
 
 
 BATCH_FIELDS = [
@@ -77,6 +78,7 @@ SIGNATURES = {
     "accfem_teams_resident": (ctypes.c_int, [c_void_p]),
     "accfem_workspace_bytes": (ctypes.c_longlong, [c_void_p]),
     "accfem_launches": (ctypes.c_int, [c_void_p]),
+    "accfem_max_batch": (ctypes.c_int, [c_void_p]),
     "accfem_grid_shape": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "accfem_grid_download": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
 }
@@ -115,7 +117,8 @@ def ptr(a):
 class Descriptors:
     """Keeps the numpy arrays behind the create-time descriptors alive."""
 
-    def __init__(self, model, mesh, cables, fixed_rows, settings, margin, uniform_load, polish_capacity=0):
+    def __init__(self, model, mesh, cables, fixed_rows, settings, margin, uniform_load, polish_capacity=0,
+                 max_batch=0, trace_slots=0):
         self.keep = []
 
         def arr(a, dt):
@@ -145,4 +148,4 @@ class Descriptors:
                                      1 if uniform_load is not None else 0, uni, float(margin), s.eps_abs, s.eps_rel,
                                      s.rho, s.sigma, s.alpha, s.beta0, s.max_iterations, s.check_interval,
                                      1 if s.adaptive_rho else 0, s.scaling_iterations, 1 if s.polish else 0,
-                                     int(polish_capacity))
+                                     int(polish_capacity), int(max_batch), int(trace_slots))

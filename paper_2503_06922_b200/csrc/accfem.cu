@@ -104,6 +104,10 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   cudaError_t alloc(size_t count) {
     if (count <= n) return cudaSuccess;
     if (p) cudaFree(p);
@@ -149,6 +153,15 @@ struct accfem_handle {
   DevBuf<double> ws;
   DevBuf<int> counter;
   long ws_stride = 0;
+  long ws_teams = 0;         // per-team slabs preallocated at create
+  int max_batch = 0;         // host-path staging capacity (scenarios per chunk)
+  long trace_slots = 0;      // host-path trace staging (scenario-frames) for coords / contacts
+  long stat_slots = 0;       // host-path trace staging (scenario-frames) for per-frame stats
+  // ordering: every launch of this handle shares the work counter and the
+  // workspace, so calls on different streams are chained through `done`
+  cudaEvent_t done = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
   // host-path staging (accfem_solve_batch_host)
   DevBuf<double> h_x0, h_ten, h_app, h_ins, h_wy, h_wf, h_rho, o_coords, o_res, o_cd, o_wy, o_wf, o_rho, o_tr;
   DevBuf<int> o_ints;
@@ -204,35 +217,36 @@ static cudaError_t build_grid(accfem_handle* h, const accfem_host::HostMesh& hm)
   const long ncell = hm.ncell;
   h->grid_cells = ncell;
   cudaError_t e;
-  DevBuf<int> count;
-  if ((e = count.alloc(ncell + 1)) != cudaSuccess) return e;
-  if ((e = h->cell_start.alloc(ncell + 1)) != cudaSuccess) return e;
-  cudaMemset(count.p, 0, (ncell + 1) * sizeof(int));
+#define GRID_OK(expr) \
+  if ((e = (expr)) != cudaSuccess) return e
+  DevBuf<int> count;  // released by its destructor on every path
+  GRID_OK(count.alloc(ncell + 1));
+  GRID_OK(h->cell_start.alloc(ncell + 1));
+  GRID_OK(cudaMemset(count.p, 0, (ncell + 1) * sizeof(int)));
   const int tb = 128, tblocks = (int)std::min<long>((hm.T + 3) / 4, 148L * 16);  // 4 warps, 1 triangle each
   k_grid_count<<<tblocks, tb>>>(g, count.p);
+  GRID_OK(cudaGetLastError());
   size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1));
+  GRID_OK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1)));
   DevBuf<char> tmp;
-  if ((e = tmp.alloc(tmp_bytes)) != cudaSuccess) return e;
-  cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1));
+  GRID_OK(tmp.alloc(tmp_bytes));
+  GRID_OK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, count.p, h->cell_start.p, (int)(ncell + 1)));
   int entries = 0;
-  if ((e = cudaMemcpy(&entries, h->cell_start.p + ncell, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess)
-    return e;
+  GRID_OK(cudaMemcpy(&entries, h->cell_start.p + ncell, sizeof(int), cudaMemcpyDeviceToHost));
   h->grid_entries = entries;
-  if ((e = h->cell_tris.alloc(std::max(entries, 1))) != cudaSuccess) return e;
+  GRID_OK(h->cell_tris.alloc(std::max(entries, 1)));
   DevBuf<int> unsorted;
-  if ((e = unsorted.alloc(std::max(entries, 1))) != cudaSuccess) return e;
-  cudaMemcpy(count.p, h->cell_start.p, (ncell + 1) * sizeof(int), cudaMemcpyDeviceToDevice);
+  GRID_OK(unsorted.alloc(std::max(entries, 1)));
+  GRID_OK(cudaMemcpy(count.p, h->cell_start.p, (ncell + 1) * sizeof(int), cudaMemcpyDeviceToDevice));
   k_grid_fill<<<tblocks, tb>>>(g, count.p, unsorted.p);
+  GRID_OK(cudaGetLastError());
   k_grid_sort<<<(int)std::min<long>((ncell + 7) / 8, 148L * 64), 256>>>(ncell, h->cell_start.p, unsorted.p,
                                                                       h->cell_tris.p);
+  GRID_OK(cudaGetLastError());
   h->launches += 3;
-  e = cudaDeviceSynchronize();
-  tmp.release();
-  count.release();
-  unsorted.release();
-  if (e == cudaSuccess) e = cudaGetLastError();
-  return e;
+  GRID_OK(cudaDeviceSynchronize());
+#undef GRID_OK
+  return cudaSuccess;
 }
 
 extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc* mesh, const accfem_settings* sd,
@@ -374,6 +388,34 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
       if (*bps < 1) *bps = 1;
     }
   }
+  // everything a solve call needs is allocated here, so solve calls never
+  // cudaMalloc: one workspace slab per resident team of either team width,
+  // and host-path staging for `max_batch` scenarios / trace slots
+  {
+    h->max_batch = sd->max_batch > 0 ? sd->max_batch : 16384;
+    h->trace_slots = sd->trace_slots > 0 ? sd->trace_slots : 1024;
+    h->stat_slots = std::max<long>(h->trace_slots, 65536);
+    long stride = (ws_doubles(N, sd->n_fixed, h->cmax) + 31) & ~31L;
+    h->ws_stride = stride;
+    h->ws_teams = std::max<long>((long)h->sms * h->blocks_per_sm, (long)h->sms * h->lat_blocks_per_sm);
+    const long Sb = h->max_batch, n = 6L * N, nf = std::max(sd->n_fixed, 1), nc = std::max(sd->n_cables, 1);
+    const long ts = h->trace_slots;
+    rc = 0;
+    if (h->ws.alloc((size_t)stride * h->ws_teams) != cudaSuccess) rc = 1;
+    if (!rc && (h->h_x0.alloc(Sb * n) || h->h_ten.alloc(Sb * nc) || h->h_app.alloc(Sb * n) || h->h_ins.alloc(Sb) ||
+                h->h_wy.alloc(Sb * N) || h->h_wf.alloc(Sb * nf) || h->h_rho.alloc(Sb)))
+      rc = 1;
+    if (!rc && (h->o_coords.alloc(Sb * n + Sb + Sb * N * 11) || h->o_ints.alloc(Sb * 4 + Sb * N * 2) ||
+                h->o_wy.alloc(Sb * N) || h->o_wf.alloc(Sb * nf) || h->o_rho.alloc(Sb)))
+      rc = 1;
+    if (!rc && h->o_tr.alloc(h->stat_slots * ACCFEM_TRACE_STATS + ts * n + ts * N * 8) != cudaSuccess) rc = 1;
+    if (!rc && cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming) != cudaSuccess) rc = 1;
+    if (rc) {
+      g_create_error = std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError());
+      accfem_destroy(h);
+      return ACCFEM_E_CUDA;
+    }
+  }
   *out = h;
   return 0;
 }
@@ -381,36 +423,28 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
 extern "C" int accfem_destroy(accfem_handle* h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
-  for (auto* b : {&h->rest, &h->rest_dir, &h->rest_len, &h->rest_frames, &h->offsets, &h->qa, &h->qb, &h->fixed_inc,
-                  &h->corners, &h->normals, &h->lo, &h->hi, &h->ws, &h->h_x0, &h->h_ten, &h->h_app, &h->h_ins,
-                  &h->h_wy, &h->h_wf, &h->h_rho, &h->o_coords, &h->o_res, &h->o_cd, &h->o_wy, &h->o_wf, &h->o_rho,
-                  &h->o_tr})
-    b->release();
-  for (auto* b : {&h->fixed_node, &h->fixed_dof, &h->fixed_row_of_dof, &h->bad, &h->cell_start,
-                  &h->cell_tris, &h->counter, &h->o_ints})
-    b->release();
-  delete h;
+  if (h->done) cudaEventSynchronize(h->done);
+  if (h->done) cudaEventDestroy(h->done);
+  delete h;  // DevBuf members free themselves
   return 0;
 }
 
-// size the workspace for `teams` resident warps
-static int ensure_ws(accfem_handle* h, long teams, int cmax) {
-  long stride = ws_doubles(h->N, h->n_fixed, cmax);
-  stride = (stride + 31) & ~31L;
-  size_t need = (size_t)stride * teams;
-  if (h->ws_stride != stride || h->ws.n < need) {
-    h->ws.release();
-    CUDA_OK(h, h->ws.alloc(need));
-    h->ws_stride = stride;
-  }
+// Calls on one handle share its work counter and workspace: a launch on a
+// stream other than the previous call's waits for that call's completion
+// event (same-stream calls are already ordered).
+static int order_on(accfem_handle* h, cudaStream_t st) {
+  if (h->has_last && h->last_stream != st) CUDA_OK(h, cudaStreamWaitEvent(st, h->done, 0));
+  return 0;
+}
+static int mark_done(accfem_handle* h, cudaStream_t st) {
+  CUDA_OK(h, cudaEventRecord(h->done, st));
+  h->last_stream = st;
+  h->has_last = true;
   return 0;
 }
 
-static long grid_blocks(accfem_handle* h, long S) {
-  long want = (S + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  long cap = (long)h->sms * h->blocks_per_sm;
-  return std::max(1L, std::min(want, cap));
-}
+// teams the preallocated workspace can host for `cmax` and a team count
+static long teams_cap(accfem_handle* h) { return h->ws_teams; }
 
 extern "C" int accfem_grid_shape(const accfem_handle* h, int32_t* dims, int64_t* n_cells, int64_t* n_entries) {
   if (!h || !dims || !n_cells || !n_entries) return ACCFEM_E_ARG;
@@ -433,6 +467,7 @@ extern "C" int accfem_grid_download(accfem_handle* h, int32_t* cell_start, int32
 extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->blocks_per_sm : 0; }
 extern "C" long long accfem_workspace_bytes(accfem_handle* h) { return h ? (long long)h->ws.n * 8 : 0; }
 extern "C" int accfem_launches(accfem_handle* h) { return h ? h->launches : 0; }
+extern "C" int accfem_max_batch(accfem_handle* h) { return h ? h->max_batch : 0; }
 
 extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void* stream) {
   if (!h || !io) return ACCFEM_E_ARG;
@@ -451,7 +486,7 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   const bool lat = (long)io->S <= (long)h->sms * h->lat_blocks_per_sm;
   const int nw = lat ? h->lat_warps : h->solve_warps;
   long blocks = std::max(1L, std::min((long)io->S, (long)h->sms * (lat ? h->lat_blocks_per_sm : h->blocks_per_sm)));
-  if (int rc = ensure_ws(h, blocks, h->cmax)) return rc;
+  blocks = std::min(blocks, teams_cap(h));
   BatchDev B;
   memset(&B, 0, sizeof(B));
   B.S = io->S;
@@ -471,12 +506,19 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   B.max_frames = io->max_frames; B.stop_on_tol = io->stop_on_tol; B.tol = io->tol;
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
   B.prof = h->prof;
+  if (int rc = order_on(h, st)) return rc;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
   CUDA_OK(h, solve_entry(nw)->launch((unsigned)blocks, (size_t)(h->hot_stride * 8), st, h->P, B, h->ws.p,
                                                   h->ws_stride, h->hot_stride));
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
-  return 0;
+  return mark_done(h, st);
+}
+
+// unit kernels: one-warp teams, at most the preallocated team count
+static long unit_blocks(accfem_handle* h, long S) {
+  long want = (S + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  return std::max(1L, std::min(want, teams_cap(h) / kWarpsPerBlock));
 }
 
 extern "C" int accfem_element_pass(accfem_handle* h, int32_t S, const double* x, double* f_int, double* k_diag,
@@ -485,14 +527,14 @@ extern "C" int accfem_element_pass(accfem_handle* h, int32_t S, const double* x,
   if (S <= 0) return 0;
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  long blocks = grid_blocks(h, S);
-  if (int rc = ensure_ws(h, blocks * kWarpsPerBlock, h->cmax)) return rc;
+  long blocks = unit_blocks(h, S);
+  if (int rc = order_on(h, st)) return rc;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
   k_element_pass<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, S, x, f_int, k_diag, k_off, frames,
                                                                      degenerate, h->ws.p, h->ws_stride, h->counter.p);
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
-  return 0;
+  return mark_done(h, st);
 }
 
 extern "C" int accfem_detect(accfem_handle* h, int32_t S, const double* x, int32_t* tri, double* gap, double* point,
@@ -502,113 +544,126 @@ extern "C" int accfem_detect(accfem_handle* h, int32_t S, const double* x, int32
   if (S <= 0) return 0;
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  long blocks = grid_blocks(h, S);
-  if (int rc = ensure_ws(h, blocks * kWarpsPerBlock, h->cmax)) return rc;
+  long blocks = unit_blocks(h, S);
+  if (int rc = order_on(h, st)) return rc;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
   k_detect<<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(h->P, S, x, tri, gap, point, h->ws.p, h->ws_stride,
                                                                h->counter.p);
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
-  return 0;
+  return mark_done(h, st);
 }
 
-// Host-pointer variant: stage inputs into handle-owned device buffers, solve,
-// copy results back.  This is the path the e2e measurement exercises.
+// Host-pointer variant: stage inputs into the handle's preallocated device
+// buffers, solve, copy results back -- in chunks of at most max_batch
+// scenarios (and as many as the trace staging holds), all on one stream.
+// This is the path the e2e measurement exercises.
 extern "C" int accfem_solve_batch_host(accfem_handle* h, const accfem_batch* io, void* stream) {
   if (!h || !io) return ACCFEM_E_ARG;
   if (io->S <= 0) return 0;
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  const long S = io->S, N = h->N, n = 6 * N, nf = h->n_fixed, nc = h->n_cables;
-  accfem_batch d = *io;
-  auto stage = [&](DevBuf<double>& b, const double* src, long cnt, const double** dst) -> int {
-    if (!src) {
-      *dst = nullptr;
+  const long N = h->N, n = 6 * N, nf = h->n_fixed, nc = h->n_cables;
+  const long tcap = io->trace_cap;
+  const bool tr_stats = io->trace_stats && tcap > 0, tr_coords = io->trace_coords && tcap > 0,
+             tr_c = io->trace_contact_node && tcap > 0;
+  long chunk = h->max_batch;
+  if (tr_stats) chunk = std::min(chunk, h->stat_slots / tcap);
+  if (tr_coords || tr_c) chunk = std::min(chunk, h->trace_slots / tcap);
+  if (chunk < 1) return fail(h, ACCFEM_E_ARG, "trace_cap exceeds the handle's trace staging (accfem_settings.trace_slots)");
+  for (long s0 = 0; s0 < io->S; s0 += chunk) {
+    const long S = std::min(chunk, (long)io->S - s0);
+    accfem_batch d = *io;
+    d.S = (int32_t)S;
+    auto stage = [&](DevBuf<double>& b, const double* src, long per, const double** dst) -> int {
+      if (!src) {
+        *dst = nullptr;
+        return 0;
+      }
+      CUDA_OK(h, cudaMemcpyAsync(b.p, src + s0 * per, S * per * sizeof(double), cudaMemcpyHostToDevice, st));
+      *dst = b.p;
       return 0;
+    };
+    int rc = 0;
+    if ((rc = stage(h->h_x0, io->x0, n, &d.x0))) return rc;
+    if ((rc = stage(h->h_ten, nc ? io->tensions : nullptr, nc, &d.tensions))) return rc;
+    if ((rc = stage(h->h_app, io->applied, n, &d.applied))) return rc;
+    if ((rc = stage(h->h_ins, io->insertion, 1, &d.insertion))) return rc;
+    if ((rc = stage(h->h_wy, io->warm_y_in, N, &d.warm_y_in))) return rc;
+    if ((rc = stage(h->h_wf, io->warm_fixed_in, nf, &d.warm_fixed_in))) return rc;
+    if ((rc = stage(h->h_rho, io->rho_in, 1, &d.rho_in))) return rc;
+    // outputs: one double slab + one int slab
+    double* p = h->o_coords.p;
+    d.coords = p; p += S * n;
+    d.residual = p; p += S;
+    d.contact_gap = p; p += S * N;
+    d.contact_multiplier = p; p += S * N;
+    d.contact_force = p; p += S * N * 3;
+    d.contact_normal = p; p += S * N * 3;
+    d.contact_point = p; p += S * N * 3;
+    int* q = h->o_ints.p;
+    d.status = q; q += S;
+    d.frames = q; q += S;
+    d.converged = q; q += S;
+    d.n_contacts = q; q += S;
+    d.contact_node = q; q += S * N;
+    d.contact_triangle = q; q += S * N;
+    d.warm_y_out = io->warm_y_out ? h->o_wy.p : nullptr;
+    d.warm_fixed_out = io->warm_fixed_out ? h->o_wf.p : nullptr;
+    d.rho_out = io->rho_out ? h->o_rho.p : nullptr;
+    d.trace_stats = nullptr;
+    d.trace_coords = nullptr;
+    d.trace_contact_node = nullptr;
+    d.trace_contact_triangle = nullptr;
+    d.trace_contact_gap = d.trace_contact_force = d.trace_contact_point = nullptr;
+    {
+      double* t = h->o_tr.p;
+      if (tr_stats) d.trace_stats = t;
+      t += h->stat_slots * ACCFEM_TRACE_STATS;
+      if (tr_coords) d.trace_coords = t;
+      t += h->trace_slots * n;
+      if (tr_c) {
+        d.trace_contact_gap = t; t += S * tcap * N;
+        d.trace_contact_force = t; t += S * tcap * N * 3;
+        d.trace_contact_point = t; t += S * tcap * N * 3;
+        int* ti = reinterpret_cast<int*>(t);
+        d.trace_contact_node = ti; ti += S * tcap * N;
+        d.trace_contact_triangle = ti;
+      }
     }
-    CUDA_OK(h, b.alloc(cnt));
-    CUDA_OK(h, cudaMemcpyAsync(b.p, src, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
-    *dst = b.p;
-    return 0;
-  };
-  int rc = 0;
-  if ((rc = stage(h->h_x0, io->x0, S * n, &d.x0))) return rc;
-  if ((rc = stage(h->h_ten, nc ? io->tensions : nullptr, S * nc, &d.tensions))) return rc;
-  if ((rc = stage(h->h_app, io->applied, S * n, &d.applied))) return rc;
-  if ((rc = stage(h->h_ins, io->insertion, S, &d.insertion))) return rc;
-  if ((rc = stage(h->h_wy, io->warm_y_in, S * N, &d.warm_y_in))) return rc;
-  if ((rc = stage(h->h_wf, io->warm_fixed_in, S * nf, &d.warm_fixed_in))) return rc;
-  if ((rc = stage(h->h_rho, io->rho_in, S, &d.rho_in))) return rc;
-  // outputs: one double slab + one int slab
-  long nd = S * n + S + S * N * 2 + S * N * 9;
-  CUDA_OK(h, h->o_coords.alloc(nd));
-  CUDA_OK(h, h->o_ints.alloc(S * 4 + S * N * 2));
-  double* p = h->o_coords.p;
-  d.coords = p; p += S * n;
-  d.residual = p; p += S;
-  d.contact_gap = p; p += S * N;
-  d.contact_multiplier = p; p += S * N;
-  d.contact_force = p; p += S * N * 3;
-  d.contact_normal = p; p += S * N * 3;
-  d.contact_point = p; p += S * N * 3;
-  int* q = h->o_ints.p;
-  d.status = q; q += S;
-  d.frames = q; q += S;
-  d.converged = q; q += S;
-  d.n_contacts = q; q += S;
-  d.contact_node = q; q += S * N;
-  d.contact_triangle = q; q += S * N;
-  if (io->warm_y_out) { CUDA_OK(h, h->o_wy.alloc(S * N)); d.warm_y_out = h->o_wy.p; }
-  if (io->warm_fixed_out) { CUDA_OK(h, h->o_wf.alloc(S * std::max(nf, 1L))); d.warm_fixed_out = h->o_wf.p; }
-  if (io->rho_out) { CUDA_OK(h, h->o_rho.alloc(S)); d.rho_out = h->o_rho.p; }
-  long tcap = io->trace_cap;
-  bool tr_stats = io->trace_stats && tcap > 0, tr_coords = io->trace_coords && tcap > 0,
-       tr_c = io->trace_contact_node && tcap > 0;
-  if (tr_stats || tr_coords || tr_c) {
-    long tn = (tr_stats ? S * tcap * ACCFEM_TRACE_STATS : 0) + (tr_coords ? S * tcap * n : 0) +
-              (tr_c ? S * tcap * N * 7 + S * tcap * N : 0);
-    CUDA_OK(h, h->o_tr.alloc(tn));
-    double* t = h->o_tr.p;
-    if (tr_stats) { d.trace_stats = t; t += S * tcap * ACCFEM_TRACE_STATS; }
-    if (tr_coords) { d.trace_coords = t; t += S * tcap * n; }
+    if ((rc = accfem_solve_batch(h, &d, stream))) return rc;
+    auto back = [&](void* dst, const void* src, size_t elem, long per) -> int {
+      if (dst && per) {
+        char* o = static_cast<char*>(dst) + (size_t)s0 * per * elem;
+        CUDA_OK(h, cudaMemcpyAsync(o, src, (size_t)S * per * elem, cudaMemcpyDeviceToHost, st));
+      }
+      return 0;
+    };
+    if ((rc = back(io->coords, d.coords, 8, n))) return rc;
+    if ((rc = back(io->residual, d.residual, 8, 1))) return rc;
+    if ((rc = back(io->status, d.status, 4, 1))) return rc;
+    if ((rc = back(io->frames, d.frames, 4, 1))) return rc;
+    if ((rc = back(io->converged, d.converged, 4, 1))) return rc;
+    if ((rc = back(io->n_contacts, d.n_contacts, 4, 1))) return rc;
+    if ((rc = back(io->contact_node, d.contact_node, 4, N))) return rc;
+    if ((rc = back(io->contact_triangle, d.contact_triangle, 4, N))) return rc;
+    if ((rc = back(io->contact_gap, d.contact_gap, 8, N))) return rc;
+    if ((rc = back(io->contact_multiplier, d.contact_multiplier, 8, N))) return rc;
+    if ((rc = back(io->contact_force, d.contact_force, 8, N * 3))) return rc;
+    if ((rc = back(io->contact_normal, d.contact_normal, 8, N * 3))) return rc;
+    if ((rc = back(io->contact_point, d.contact_point, 8, N * 3))) return rc;
+    if (io->warm_y_out && (rc = back(io->warm_y_out, d.warm_y_out, 8, N))) return rc;
+    if (io->warm_fixed_out && (rc = back(io->warm_fixed_out, d.warm_fixed_out, 8, nf))) return rc;
+    if (io->rho_out && (rc = back(io->rho_out, d.rho_out, 8, 1))) return rc;
+    if (tr_stats && (rc = back(io->trace_stats, d.trace_stats, 8, tcap * ACCFEM_TRACE_STATS))) return rc;
+    if (tr_coords && (rc = back(io->trace_coords, d.trace_coords, 8, tcap * n))) return rc;
     if (tr_c) {
-      d.trace_contact_gap = t; t += S * tcap * N;
-      d.trace_contact_force = t; t += S * tcap * N * 3;
-      d.trace_contact_point = t; t += S * tcap * N * 3;
-      int* ti = reinterpret_cast<int*>(t);
-      d.trace_contact_node = ti; ti += S * tcap * N;
-      d.trace_contact_triangle = ti;
+      if ((rc = back(io->trace_contact_node, d.trace_contact_node, 4, tcap * N))) return rc;
+      if ((rc = back(io->trace_contact_triangle, d.trace_contact_triangle, 4, tcap * N))) return rc;
+      if ((rc = back(io->trace_contact_gap, d.trace_contact_gap, 8, tcap * N))) return rc;
+      if ((rc = back(io->trace_contact_force, d.trace_contact_force, 8, tcap * N * 3))) return rc;
+      if ((rc = back(io->trace_contact_point, d.trace_contact_point, 8, tcap * N * 3))) return rc;
     }
-  }
-  if ((rc = accfem_solve_batch(h, &d, stream))) return rc;
-  auto back = [&](void* dst, const void* src, size_t bytes) -> int {
-    if (dst && bytes) CUDA_OK(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
-    return 0;
-  };
-  if ((rc = back(io->coords, d.coords, S * n * 8))) return rc;
-  if ((rc = back(io->residual, d.residual, S * 8))) return rc;
-  if ((rc = back(io->status, d.status, S * 4))) return rc;
-  if ((rc = back(io->frames, d.frames, S * 4))) return rc;
-  if ((rc = back(io->converged, d.converged, S * 4))) return rc;
-  if ((rc = back(io->n_contacts, d.n_contacts, S * 4))) return rc;
-  if ((rc = back(io->contact_node, d.contact_node, S * N * 4))) return rc;
-  if ((rc = back(io->contact_triangle, d.contact_triangle, S * N * 4))) return rc;
-  if ((rc = back(io->contact_gap, d.contact_gap, S * N * 8))) return rc;
-  if ((rc = back(io->contact_multiplier, d.contact_multiplier, S * N * 8))) return rc;
-  if ((rc = back(io->contact_force, d.contact_force, S * N * 24))) return rc;
-  if ((rc = back(io->contact_normal, d.contact_normal, S * N * 24))) return rc;
-  if ((rc = back(io->contact_point, d.contact_point, S * N * 24))) return rc;
-  if (io->warm_y_out && (rc = back(io->warm_y_out, d.warm_y_out, S * N * 8))) return rc;
-  if (io->warm_fixed_out && (rc = back(io->warm_fixed_out, d.warm_fixed_out, S * nf * 8))) return rc;
-  if (io->rho_out && (rc = back(io->rho_out, d.rho_out, S * 8))) return rc;
-  if (tr_stats && (rc = back(io->trace_stats, d.trace_stats, S * tcap * ACCFEM_TRACE_STATS * 8))) return rc;
-  if (tr_coords && (rc = back(io->trace_coords, d.trace_coords, S * tcap * n * 8))) return rc;
-  if (tr_c) {
-    if ((rc = back(io->trace_contact_node, d.trace_contact_node, S * tcap * N * 4))) return rc;
-    if ((rc = back(io->trace_contact_triangle, d.trace_contact_triangle, S * tcap * N * 4))) return rc;
-    if ((rc = back(io->trace_contact_gap, d.trace_contact_gap, S * tcap * N * 8))) return rc;
-    if ((rc = back(io->trace_contact_force, d.trace_contact_force, S * tcap * N * 24))) return rc;
-    if ((rc = back(io->trace_contact_point, d.trace_contact_point, S * tcap * N * 24))) return rc;
   }
   CUDA_OK(h, cudaStreamSynchronize(st));
   return 0;

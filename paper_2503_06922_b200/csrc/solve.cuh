@@ -721,7 +721,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
   PARFOR(j, n) gnorm = fmax(gnorm, fabs(ws.g[j]));
   gnorm = team.max(gnorm);
   PROF_T0(t_ruiz);
-  double c = ruiz(team, P, F, ws);
+  const double cost = ruiz(team, P, F, ws);  // Ruiz cost factor
   PROF_ADD(ws, PF_RUIZ, t_ruiz);
   double rho_bar = fmin(fmax(rho_in, kRhoMin), kRhoMax);
   double rho_eq = fmin(fmax(rho_bar * kRhoEqFactor, kRhoMin), kRhoMax);
@@ -760,7 +760,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     double y0;
     if (r < nf) y0 = has_wfix ? ws.wfix[r] : 0.0;
     else y0 = ws.warm[ws.cnode[r - nf]];
-    ws.y[r] = c * y0 / ws.e[r];
+    ws.y[r] = cost * y0 / ws.e[r];
     ws.z[r] = fmin(fmax(0.0, ws.ls[r]), ws.us[r]);
   }
   team.sync();
@@ -819,12 +819,12 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
     team.sync();
     if (k <= 8 || k % S.check_interval == 0 || k == S.max_iterations) {
       PROF_T0(t_chk);
-      Residuals R = unscaled_residuals(team, P, F, ws, c, gnorm);
+      Residuals R = unscaled_residuals(team, P, F, ws, cost, gnorm);
       team.sync();
       PROF_ADD(ws, PF_CHECK, t_chk);
       if (R.pri <= S.eps_abs + S.eps_rel * R.ps && R.dua <= S.eps_abs + S.eps_rel * R.ds) break;
       if (k % S.check_interval == 0) {
-        infeas = infeasible(team, P, F, ws, c);
+        infeas = infeasible(team, P, F, ws, cost);
         team.sync();
         if (infeas) break;
         if (k == S.check_interval) {
@@ -840,7 +840,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
 #endif
   if (k > S.max_iterations) k = S.max_iterations;
   if (infeas) return ST_INFEASIBLE;
-  Residuals R = unscaled_residuals(team, P, F, ws, c, gnorm);
+  Residuals R = unscaled_residuals(team, P, F, ws, cost, gnorm);
   PARFOR(j, n) ws.dx[j] = ws.tmp[j];  // tmp holds d o xs
   team.sync();
   res.pri = R.pri;

@@ -82,7 +82,7 @@ class Engine:
     """Single-writer stepping loop over one robot/mesh/constraint setup."""
 
     def __init__(self, model, mesh=None, cables=(), fixed_specs=(), settings=None, margin=1e-4,
-                 uniform_load=None, device=None, polish_capacity=0):
+                 uniform_load=None, device=None, polish_capacity=0, max_batch=0):
         self.model = model
         self.mesh = mesh
         self.cables = list(cables)
@@ -107,7 +107,7 @@ class Engine:
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
         self._lib = _lib.load()
         self._desc = _lib.Descriptors(model, mesh, self.cables, self._rows, self.settings, self.margin,
-                                      self.uniform_load, polish_capacity)
+                                      self.uniform_load, polish_capacity, max_batch)
         handle = ctypes.c_void_p()
         rc = self._lib.accfem_create(ctypes.byref(self._desc.model), ctypes.byref(self._desc.mesh),
                                      ctypes.byref(self._desc.settings), self.device.index, ctypes.byref(handle))
@@ -120,6 +120,10 @@ class Engine:
                 raise MeshError(msg)
             raise DeviceError(f"accfem_create failed ({rc}): {msg}")
         self._h = handle
+        # reference callers that build their own initial record read the
+        # engine's broad-phase tree (engine.py:96, 319-338); None makes
+        # detect_contacts build its own (the device grid lives in the handle)
+        self._tree = None
         # cross-frame solver state (engine.py:100-103)
         self._warm_y = np.zeros(model.node_count)
         self._warm_fixed = None
@@ -291,6 +295,44 @@ class Engine:
         raise EngineError(f"static mode did not reach |dx| <= {tol} in {max_frames} frames "
                           f"(last |dx| = {records[-1].dx_norm:.3e})")
 
+    # -- batch input checks ------------------------------------------------------
+    def _batch_input(self, a, shape, name, host):
+        """float64, C-contiguous, the declared shape, and on the right side of the
+        boundary: numpy for the host path, a CUDA tensor on this engine's device
+        for the device path (converted if needed; a host pointer must never reach
+        a kernel)."""
+        if a is None:
+            return None
+        import torch
+
+        if host:
+            if isinstance(a, torch.Tensor):
+                a = a.detach().cpu().numpy()
+            a = np.ascontiguousarray(a, dtype=np.float64)
+        else:
+            if not isinstance(a, torch.Tensor):
+                a = torch.as_tensor(np.asarray(a, dtype=np.float64))
+            a = a.to(device=self.device, dtype=torch.float64).contiguous()
+        if tuple(a.shape) != tuple(shape):
+            raise DomainError(f"{name} must have shape {tuple(shape)}, got {tuple(a.shape)}")
+        return a
+
+    def _check_out(self, out, S, host):
+        import torch
+
+        ref = self.allocate_batch(0, host=host)
+        for name in ("coords", "status", "frames", "converged", "residual", "n_contacts", "contact_node",
+                     "contact_triangle", "contact_gap", "contact_multiplier", "contact_force", "contact_normal",
+                     "contact_point"):
+            a, r = getattr(out, name), getattr(ref, name)
+            want = (S,) + tuple(r.shape[1:])
+            if tuple(a.shape) != want or a.dtype != r.dtype:
+                raise DomainError(f"out.{name} must be {r.dtype} of shape {want}")
+            if host and not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+                raise DomainError(f"out.{name} must be a C-contiguous numpy array for a host call")
+            if not host and not (isinstance(a, torch.Tensor) and a.device == self.device and a.is_contiguous()):
+                raise DomainError(f"out.{name} must be a contiguous tensor on {self.device}")
+
     # -- batch -----------------------------------------------------------------
     def allocate_batch(self, S, host=False):
         """Output buffers for S scenarios (torch on device, or numpy if host)."""
@@ -308,48 +350,58 @@ class Engine:
                            contact_force=z((S, N, 3)), contact_normal=z((S, N, 3)), contact_point=z((S, N, 3)))
 
     def solve_static_batch(self, x0, tensions=None, applied=None, insertion=None, tol=1e-9, max_frames=5000,
-                           out=None, stream=None, host=None):
+                           out=None, stream=None, host=None, trace_frames=0):
         """run_static of S independent scenarios, each from a fresh Engine state.
 
         Inputs are (S, 6N) / (S, n_cables) arrays: torch CUDA tensors (device
         path, async on `stream`) or numpy arrays (host path: copies inside the
         call).  Status codes per scenario follow include/accfem.h.
+        `trace_frames` > 0 also records the first `trace_frames` frames' stats
+        of every scenario (FrameRecord fields, include/accfem.h
+        ACCFEM_TRACE_STATS layout) into `out.trace_stats` (S, trace_frames, 12).
         """
         import torch
 
         if host is None:
             host = isinstance(x0, np.ndarray)
         S = int(x0.shape[0])
-        n = self.model.dof_count
-        if x0.shape != (S, n):
-            raise DomainError(f"x0 must have shape (S, {n})")
-        if tensions is not None and self.cables:
-            if tensions.shape != (S, len(self.cables)):
-                raise DomainError("one tension per cable required")
+        n, nca = self.model.dof_count, len(self.cables)
+        x0 = self._batch_input(x0, (S, n), "x0", host)
+        tensions = self._batch_input(tensions, (S, nca), "tensions", host) if self.cables else None
+        if tensions is not None and bool((tensions < 0).any()):
+            raise DomainError("cable tensions must be >= 0 (cables cannot push)")
+        applied = self._batch_input(applied, (S, n), "applied", host)
+        insertion = self._batch_input(insertion, (S,), "insertion", host)
         if out is None:
             out = self.allocate_batch(S, host=host)
+        else:
+            self._check_out(out, S, host)
         desc = _lib.BatchDesc()
         desc.S = S
         keep = []
 
-        def put(name, a, dtype=None):
+        def put(name, a):
             if a is None:
                 return
-            if host:
-                a = np.ascontiguousarray(a, dtype=dtype or np.float64)
-            else:
-                a = a.contiguous()
             keep.append(a)
             setattr(desc, name, _lib.ptr(a))
 
         put("x0", x0)
-        put("tensions", tensions if self.cables else None)
+        put("tensions", tensions)
         put("applied", applied)
         put("insertion", insertion)
         for name in ("coords", "status", "frames", "converged", "residual", "n_contacts", "contact_node",
                      "contact_triangle", "contact_gap", "contact_multiplier", "contact_force", "contact_normal",
                      "contact_point"):
             setattr(desc, name, _lib.ptr(getattr(out, name)))
+        if trace_frames > 0:
+            if host:
+                out.trace_stats = np.zeros((S, int(trace_frames), _lib.TRACE_STATS))
+            else:
+                out.trace_stats = torch.zeros((S, int(trace_frames), _lib.TRACE_STATS), dtype=torch.float64,
+                                              device=self.device)
+            desc.trace_cap = int(trace_frames)
+            desc.trace_stats = _lib.ptr(out.trace_stats)
         desc.max_frames = int(max_frames)
         desc.stop_on_tol = 1
         desc.tol = float(tol)
@@ -383,15 +435,24 @@ class Engine:
         import torch
 
         S, N = int(x.shape[0]), self.model.node_count
-        nf = len(self._rows)
+        n, nf, nca = self.model.dof_count, len(self._rows), len(self.cables)
         if state is None:
             state = self.initial_batch_state(S)
+        for name, a, shape in (("state.warm_y", state.warm_y, (S, N)), ("state.rho", state.rho, (S,)),
+                               ("state.warm_fixed", state.warm_fixed, (S, nf))):
+            if a is not None and (tuple(a.shape) != shape or a.dtype != torch.float64 or a.device != self.device):
+                raise DomainError(f"{name} must be float64 {shape} on {self.device}")
         out = self.allocate_batch(S)
         stats = torch.zeros((S, 1, _lib.TRACE_STATS), dtype=torch.float64, device=self.device)
         new = BatchState(warm_y=torch.zeros_like(state.warm_y),
                          warm_fixed=torch.zeros((S, max(nf, 1)), dtype=torch.float64, device=self.device),
                          rho=torch.zeros_like(state.rho))
-        keep = [t.contiguous() if t is not None else None for t in (x, tensions, applied, insertion)]
+        keep = [self._batch_input(x, (S, n), "x", False),
+                self._batch_input(tensions, (S, nca), "tensions", False) if self.cables else None,
+                self._batch_input(applied, (S, n), "applied", False),
+                self._batch_input(insertion, (S,), "insertion", False)]
+        wf = None if state.warm_fixed is None else state.warm_fixed.contiguous()
+        keep.append(wf)
         desc = _lib.BatchDesc()
         desc.S = S
         desc.x0 = _lib.ptr(keep[0])
@@ -399,7 +460,7 @@ class Engine:
         desc.applied = _lib.ptr(keep[2])
         desc.insertion = _lib.ptr(keep[3])
         desc.warm_y_in = _lib.ptr(state.warm_y)
-        desc.warm_fixed_in = _lib.ptr(state.warm_fixed)
+        desc.warm_fixed_in = _lib.ptr(wf)
         desc.rho_in = _lib.ptr(state.rho)
         for name in ("coords", "status", "frames", "converged", "residual", "n_contacts", "contact_node",
                      "contact_triangle", "contact_gap", "contact_multiplier", "contact_force", "contact_normal",

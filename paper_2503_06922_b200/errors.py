@@ -1,49 +1,63 @@
 """Exception taxonomy of the reference, kept verbatim in meaning.
 
 Mirrors `cablefem/errors.py:4-44` so callers that catch the reference's
-exceptions keep working.  The device path reports a per-scenario status code
-(`STATUS_*` below, identical to `include/accfem.h`) and the host wrapper turns
-it back into the matching exception for single-scenario calls.
+exceptions keep working.  When the reference package `cablefem` is importable
+(installed, or on sys.path) every class here also SUBCLASSES the reference
+class of the same name, so `except cablefem.errors.EngineError` catches a
+device failure raised by this package.  The device path reports a
+per-scenario status code (`STATUS_*` below, identical to `include/accfem.h`)
+and the host wrapper turns it back into the matching exception for
+single-scenario calls.
 """
 
+try:  # the reference's own classes, when present (drop-in for callers that catch them)
+    from cablefem import errors as _ref
+except Exception:  # noqa: BLE001 - reference not installed: standalone taxonomy
+    _ref = None
 
-class CableFemError(Exception):
+
+def _bases(name, *own):
+    ref = getattr(_ref, name, None) if _ref is not None else None
+    return (ref, *own) if ref is not None else own
+
+
+class CableFemError(*_bases("CableFemError", Exception)):
     """Root of every simulator error (reference `errors.py:4`)."""
 
 
-class DomainError(CableFemError, ValueError):
+class DomainError(*_bases("DomainError", CableFemError, ValueError)):
     """Argument outside its mathematical domain (reference `errors.py:8`)."""
 
 
-class DegenerateElementError(CableFemError):
+class DegenerateElementError(*_bases("DegenerateElementError", CableFemError)):
     """Coincident element end nodes (reference `errors.py:12`)."""
 
 
-class MeshError(CableFemError):
+class MeshError(*_bases("MeshError", CableFemError)):
     """Empty / malformed mesh (reference `errors.py:16`)."""
 
 
-class ScenarioError(CableFemError):
+class ScenarioError(*_bases("ScenarioError", CableFemError)):
     """Scenario description invalid (reference `errors.py:20`)."""
 
 
-class NonConvergenceError(CableFemError):
+class NonConvergenceError(*_bases("NonConvergenceError", CableFemError)):
     """ADMM ran out of iterations; carries the last iterate (reference `errors.py:24-32`)."""
 
     def __init__(self, message, result=None):
-        super().__init__(message)
+        Exception.__init__(self, message)
         self.result = result
 
 
-class InfeasibleError(CableFemError):
+class InfeasibleError(*_bases("InfeasibleError", CableFemError)):
     """Primal infeasibility certificate found (reference `errors.py:35-41`)."""
 
     def __init__(self, message, certificate=None):
-        super().__init__(message)
+        Exception.__init__(self, message)
         self.certificate = certificate
 
 
-class EngineError(CableFemError):
+class EngineError(*_bases("EngineError", CableFemError)):
     """A frame failed after the retry, or static mode ran out of frames (reference `errors.py:44`)."""
 
 

@@ -130,9 +130,11 @@ def cfg3(n_scenarios=1):
     return cfg_tube(101, 0.47, 20, "cfg3", n_scenarios)
 
 
-def constriction(node_count, target, name, n_scenarios=1, load_per_node=0.02, margin=1e-4):
-    """Floor strip under the loaded nodes (reference bench.py:51-71)."""
-    model = straight_model(node_count, 0.47 * node_count / 100.0, material_a())
+def constriction(node_count, target, name, n_scenarios=1, load_per_node=0.02, margin=1e-4, length=None):
+    """Floor strip under the loaded nodes (reference bench.py:51-71).
+    `length` overrides the bench's constant-l0 length (0.47 m per 100 nodes)."""
+    total = 0.47 * node_count / 100.0 if length is None else float(length)
+    model = straight_model(node_count, total, material_a())
     l0 = model.element_rest_length
     loaded = np.arange(1, target + 1)
     x_lo = loaded[0] * l0 - 0.49 * l0
@@ -192,6 +194,28 @@ def cfg4(n_scenarios=65536, seed=CFG4_SEED, start=0):
     return Workload("cfg4", model, base.mesh, base.fixed_specs, base.cables, base.settings,
                     base.margin, x0, tensions, applied, max_frames=400,
                     meta={"seed": seed, "start": start})
+
+
+def cfg5_fine(n_scenarios=1):
+    """cfg5's fine discretisation (L = 0.47 m, l0 = 0.47 mm): the reference's
+    ADMM stalls and the frame fails twice -> EngineError at frame 0
+    (SURVEY Appendix C).  A parity case of failure, not a throughput config."""
+    return constriction(1001, 200, "cfg5_fine", n_scenarios, length=0.47)
+
+
+def infeasible_press(n_scenarios=1, push=1e-3):
+    """Base node clamped with a prescribed increment `push` m INTO a floor it
+    already touches: the selector row contradicts the node's contact row, so
+    ADMM's certificate test (solver.py:424-446) raises InfeasibleError."""
+    model = straight_model(21, 0.07, material_a())
+    l0 = model.element_rest_length
+    margin = 1e-4
+    floor = make_rectangle((0.0, 0.0, -0.4 * margin), 0.98 * l0, 1.0, normal_axis="z")
+    applied = None
+    x0 = np.tile(model.rest_configuration, (n_scenarios, 1))
+    fixed = [FixedNodeSpec(0, prescribed_increment=(0.0, 0.0, -push, 0.0, 0.0, 0.0))]
+    return Workload("infeasible", model, floor, fixed, [], SolverSettings(), margin, x0, None, applied,
+                    max_frames=50)
 
 
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg3p": cfg3p, "cfg4": cfg4, "cfg5": cfg5}

@@ -33,31 +33,74 @@ def engine_for(w, **kw):
     return Engine(**w.engine_kwargs(), device=0, **kw)
 
 
-def device_solve(w, host=False):
+def device_solve(w, host=False, trace=True):
+    """run_static of every scenario of w through the C ABI, with per-frame traces."""
     eng = engine_for(w)
+    cap = min(int(w.max_frames), 512) if trace else 0
     if host:
-        res = eng.solve_static_batch(w.x0, w.tensions, w.applied, tol=w.tol, max_frames=w.max_frames)
+        res = eng.solve_static_batch(w.x0, w.tensions, w.applied, tol=w.tol, max_frames=w.max_frames,
+                                     trace_frames=cap)
         return res, eng
     t = lambda a: None if a is None else torch.tensor(a, device=DEV)  # noqa: E731
-    res = eng.solve_static_batch(t(w.x0), t(w.tensions), t(w.applied), tol=w.tol, max_frames=w.max_frames)
+    res = eng.solve_static_batch(t(w.x0), t(w.tensions), t(w.applied), tol=w.tol, max_frames=w.max_frames,
+                                 trace_frames=cap)
     torch.cuda.synchronize()
     return res.to_numpy(), eng
 
 
+# ACCFEM_TRACE_STATS columns (include/accfem.h)
+T_DX, T_SCALE, T_PEN, T_COMPL, T_RESID, T_ITERS, T_NC, T_CONV, T_RETRIED = range(9)
+
+
+def check_forces(got, ref, tag):
+    """Contact forces per contact: |f - f_ref| <= 1e-5 |f_ref| (+1e-10 of the largest, for
+    contacts whose force vanishes)."""
+    assert got.shape == ref.shape, tag
+    if not ref.size:
+        return
+    err = np.linalg.norm(got - ref, axis=1)
+    scale = np.linalg.norm(ref, axis=1)
+    bound = FORCE_TOL * scale + 1e-10 * scale.max()
+    assert np.all(err <= bound), (tag, float((err / np.maximum(scale, 1e-300)).max()))
+
+
+def check_frames(g, tag, tr, frames):
+    """Per-frame FrameRecord parity: ADMM iterations, n_c, retried equal; dx_norm,
+    actuation_scale, residual at 1e-6 relative; penetration and complementarity."""
+    its = g[f"{tag}_iterations"]
+    cap = min(frames, tr.shape[0])
+    assert np.array_equal(tr[:cap, T_ITERS].astype(np.int64), its[:cap].astype(np.int64)), tag
+    assert np.array_equal(tr[:cap, T_NC].astype(np.int64), g[f"{tag}_n_c"][:cap].astype(np.int64)), tag
+    assert np.array_equal(tr[:cap, T_RETRIED].astype(bool), g[f"{tag}_retried"][:cap].astype(bool)), tag
+    dx = g[f"{tag}_dx_norm"][:cap]
+    # frames that end a solve move by roundoff only (dx ~ 1e-12): absolute floor 1e-10 (tol is 1e-9)
+    assert np.all(np.abs(tr[:cap, T_DX] - dx) <= 1e-6 * dx + 1e-10), tag
+    res = g[f"{tag}_frame_residual"][:cap]
+    assert np.all(np.abs(tr[:cap, T_RESID] - res) <= 1e-6 * np.maximum(1.0, res)), tag
+    sc = g[f"{tag}_frame_scale"][:cap]
+    assert np.all(np.abs(tr[:cap, T_SCALE] - sc) <= 1e-6 * sc), tag
+    if f"{tag}_frame_max_pen" in g:
+        pen = g[f"{tag}_frame_max_pen"][:cap]
+        assert np.all(np.abs(tr[:cap, T_PEN] - pen) <= 1e-6 * pen + 1e-12), tag
+        cw = g[f"{tag}_frame_compl_worst"][:cap]
+        assert np.all(np.abs(tr[:cap, T_COMPL] - cw) <= 1e-8), tag
+
+
 def check_against_golden(g, tag, r, i):
-    assert int(r.status[i]) == int(g[f"{tag}_status"]), tag
+    assert int(r.status[i]) == int(g[f"{tag}_status"]), (tag, int(r.status[i]), int(g[f"{tag}_status"]))
     if int(r.status[i]) != 0:
         return
-    assert int(r.frames[i]) == int(g[f"{tag}_frames"]), tag
+    frames = int(g[f"{tag}_frames"])
+    assert int(r.frames[i]) == frames, tag
     nc = int(r.n_contacts[i])
     assert np.array_equal(r.contact_node[i, :nc], g[f"{tag}_contact_nodes"]), tag
     assert np.array_equal(r.contact_triangle[i, :nc], g[f"{tag}_contact_tris"]), tag
     ref = g[f"{tag}_coords"]
     assert np.abs(r.coords[i] - ref).max() <= COORD_TOL * np.abs(ref).max(), tag
-    fr = g[f"{tag}_contact_forces"]
-    if fr.size:
-        assert np.abs(r.contact_force[i, :nc] - fr).max() <= FORCE_TOL * np.abs(fr).max(), tag
+    check_forces(r.contact_force[i, :nc], g[f"{tag}_contact_forces"], tag)
     assert abs(float(r.residual[i]) - float(g[f"{tag}_residual"])) <= 1e-6 * max(1.0, float(g[f"{tag}_residual"]))
+    if r.trace_stats is not None:
+        check_frames(g, tag, r.trace_stats[i], frames)
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg2", "cfg5"])
@@ -67,6 +110,68 @@ def test_static_solves_match_reference_goldens(golden, name):
     r, _ = device_solve(w)
     for i in range(w.size):
         check_against_golden(g, f"{name}_{i}", r, i)
+
+
+def _status_case(tag):
+    """The workload of a status.npz case (tests/golden/make_golden_status.py)."""
+    import dataclasses
+    make = {
+        "retry_ok": lambda: (scenarios.cfg4(1), dict(max_iterations=300)),
+        "retry_fail0": lambda: (scenarios.cfg3(1), dict(max_iterations=30)),
+        "retry_fail9": lambda: (scenarios.cfg3(1), dict(max_iterations=200)),
+        "infeasible": lambda: (scenarios.infeasible_press(1), {}),
+        "cfg5_fine": lambda: (scenarios.cfg5_fine(1), {}),
+        "cfg5_250": lambda: (scenarios.cfg5(1, target=250), {}),
+        "cfg4_984": lambda: (scenarios.cfg4(1, start=984), {}),
+        "cfg4_5450": lambda: (scenarios.cfg4(1, start=5450), {}),
+        "maxframes3": lambda: (scenarios.cfg3(1), {}),
+    }[tag]
+    w, kw = make()
+    if kw:
+        w.settings = dataclasses.replace(w.settings, **kw)
+    if tag == "maxframes3":
+        w.max_frames = 3
+    return w
+
+
+STATUS_CASES = ["retry_ok", "retry_fail0", "retry_fail9", "infeasible", "cfg5_fine", "cfg5_250", "cfg4_984",
+                "cfg4_5450", "maxframes3"]
+
+
+@pytest.mark.parametrize("tag", STATUS_CASES)
+def test_status_and_failure_modes_match_reference(golden, tag):
+    """Failure-status parity against the real reference:
+    retry -> success, retry -> EngineError at frames 0 and 9, InfeasibleError,
+    the fine-l0 cfg5 EngineError, cfg5 with 250 contacts, the two cfg4 bench
+    scenarios that exhaust 400 frames, and max_frames=3."""
+    g = golden("status.npz")
+    w = _status_case(tag)
+    r, _ = device_solve(w)
+    check_against_golden(g, tag, r, 0)
+    st = int(g[f"{tag}_status"])
+    if st in (6,) and f"{tag}_fail_frame" in g:
+        # EngineError after the retry at the reference's frame: the frames before it completed
+        assert int(r.frames[0]) == int(g[f"{tag}_fail_frame"]), (tag, int(r.frames[0]))
+    if tag == "retry_ok":
+        assert int(g[f"{tag}_retried"].sum()) == 1 and int(r.trace_stats[0, :, T_RETRIED].sum()) == 1
+
+
+def test_single_scenario_api_raises_reference_exception_classes():
+    """Engine.run_static raises the taxonomy's classes for device statuses (errors.py:4-44)."""
+    import dataclasses
+
+    from paper_2503_06922_b200.engine import Engine
+    from paper_2503_06922_b200.errors import EngineError, InfeasibleError
+    w = scenarios.infeasible_press(1)
+    eng = Engine(**w.engine_kwargs(), device=0)
+    with pytest.raises(InfeasibleError):
+        eng.run_static(StepInputs(), x0=Configuration(w.x0[0].copy()), tol=w.tol, max_frames=w.max_frames)
+    w = scenarios.cfg3(1)
+    w.settings = dataclasses.replace(w.settings, max_iterations=30)
+    eng = Engine(**w.engine_kwargs(), device=0)
+    with pytest.raises(EngineError):
+        eng.run_static(StepInputs(tensions=w.tensions[0], applied_force=w.applied[0]),
+                       x0=Configuration(w.x0[0].copy()), tol=w.tol, max_frames=w.max_frames)
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg4"])
@@ -96,21 +201,32 @@ def test_cfg4_batch_matches_reference_goldens(golden):
 
 
 def test_cfg4_batch_matches_oracle_and_host_path():
+    """24 cfg4 scenarios (a shard away from the golden ones) against the CPU oracle:
+    status, frames, per-frame ADMM iterations and n_c, contact sets, coords, forces;
+    the host-buffer C ABI path gives the identical result."""
     w = scenarios.cfg4(48, start=100)
     r, _ = device_solve(w)
     rh, _ = device_solve(w, host=True)
-    ref = O.solve_workload(w, indices=range(0, 48, 6))
-    for j, i in enumerate(range(0, 48, 6)):
+    picks = list(range(0, 48, 2))
+    ref = O.solve_workload(w, indices=picks)
+    for j, i in enumerate(picks):
         o = ref[j]
         assert int(r.status[i]) == o["status"]
+        if o["status"] != 0:
+            continue
         assert int(r.frames[i]) == o["frames"]
+        f = o["frames"]
+        assert np.array_equal(r.trace_stats[i, :f, T_ITERS].astype(np.int64), o["iterations"].astype(np.int64))
+        assert np.array_equal(r.trace_stats[i, :f, T_NC].astype(np.int64), o["n_c"].astype(np.int64))
         nc = int(r.n_contacts[i])
         assert np.array_equal(r.contact_node[i, :nc], o["contact_nodes"])
         assert np.array_equal(r.contact_triangle[i, :nc], o["contact_tris"])
         assert np.abs(r.coords[i] - o["coords"]).max() <= COORD_TOL * np.abs(o["coords"]).max()
+        check_forces(r.contact_force[i, :nc], o["contact_forces"], f"cfg4[{100 + i}]")
     # host-buffer C ABI path is the same computation
     assert np.array_equal(rh.coords, r.coords)
     assert np.array_equal(rh.frames, r.frames)
+    assert np.array_equal(rh.trace_stats, r.trace_stats)
 
 
 def test_run_static_records_match_oracle_iteration_counts():
@@ -220,13 +336,6 @@ def test_degenerate_element_status():
     w.x0 = x0
     r, _ = device_solve(w)
     assert int(r.status[0]) == 2  # DegenerateElementError
-
-
-def test_max_frames_status():
-    w = scenarios.cfg3(1)
-    w.max_frames = 3
-    r, _ = device_solve(w)
-    assert int(r.status[0]) == 7  # EngineError (static mode did not converge)
 
 
 def test_empty_batch_and_launch_count():
