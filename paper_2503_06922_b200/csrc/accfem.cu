@@ -31,6 +31,8 @@ constexpr int kWarpsPerBlock = 4;
 // parallel phases run twice as wide; measured p50 -15% at batch 1)
 constexpr int kTeamWarps = 2;
 constexpr int kLatencyTeamWarps = 4;
+// latency mode with cyclic reduction: one CTA of kCrTeamWarps warps per scenario (ksolve_cr.cu)
+constexpr int kCrTeamWarps = 8;
 
 __global__ void k_model_setup(int N, const double* rest, double* rest_dir, double* rest_len, double* rest_frames,
                               double* offsets, double* qa, double* qb, int* bad) {
@@ -41,10 +43,10 @@ __global__ void k_model_setup(int N, const double* rest, double* rest_dir, doubl
 
 // k_solve<NW> lives in ksolve.cuh, one translation unit per team width
 // (ksolve_<NW>.cu, compiled in parallel); this table reaches them.
-static const KSolveEntry* solve_entry(int nw) {
-  static const KSolveEntry table[] = {ksolve_entry_2(), ksolve_entry_4()};
+static const KSolveEntry* solve_entry(int nw, bool cr = false) {
+  static const KSolveEntry table[] = {ksolve_entry_2(), ksolve_entry_4(), ksolve_entry_cr()};
   for (const KSolveEntry& e : table)
-    if (e.nw == nw) return &e;
+    if (e.nw == nw && e.cr == cr) return &e;
   return nullptr;
 }
 
@@ -140,6 +142,9 @@ struct accfem_handle {
   int lat_blocks_per_sm = 0; // the same for latency mode
   int lat_warps = 0;
   long hot_stride = 0;       // doubles of shared memory per warp (0: global mode)
+  int cr_blocks_per_sm = 0;  // the cyclic-reduction latency kernel (0: disabled)
+  long cr_hot_stride = 0;
+  int force_mode = 0;        // test hook ACCFEM_MODE: 1 cr, 2 4-warp teams, 3 2-warp teams (0: by batch size)
   int launches = 0;
   std::string err;
   Problem P;
@@ -387,17 +392,37 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, 32 * nw, in_smem ? hot * 8 : 0);
       if (*bps < 1) *bps = 1;
     }
+    // latency mode: one 16-warp CTA per scenario, cyclic reduction, hot set in shared memory
+    const char* no_cr = getenv("ACCFEM_NO_CR");
+    const char* mode = getenv("ACCFEM_MODE");
+    if (mode) h->force_mode = !strcmp(mode, "cr") ? 1 : !strcmp(mode, "team4") ? 2 : !strcmp(mode, "team2") ? 3 : 0;
+    long hot_cr = (ws_hot_doubles(N, sd->n_fixed, true) + 15) & ~15L;
+    const KSolveEntry* ce = solve_entry(kCrTeamWarps, true);
+    h->cr_blocks_per_sm = 0;
+    if (ce && !(no_cr && no_cr[0] == '1')) {
+      const bool cr_smem = hot_cr * 8 <= max_smem && !(force_global && force_global[0] == '1');
+      h->cr_hot_stride = cr_smem ? hot_cr : 0;
+      if (cr_smem) cudaFuncSetAttribute(ce->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(hot_cr * 8));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->cr_blocks_per_sm, ce->kernel, 32 * kCrTeamWarps,
+                                                    cr_smem ? hot_cr * 8 : 0);
+    }
   }
   // everything a solve call needs is allocated here, so solve calls never
   // cudaMalloc: one workspace slab per resident team of either team width,
   // and host-path staging for `max_batch` scenarios / trace slots
   {
-    h->max_batch = sd->max_batch > 0 ? sd->max_batch : 16384;
+    {
+      // default: 16384 scenarios, at most ~2 GiB of staging for large models
+      const long per = 8L * (3 * 6L * N + 2 + 13L * N) + 4L * (4 + 2L * N);
+      h->max_batch = sd->max_batch > 0 ? sd->max_batch : (int)std::max(1L, std::min(16384L, (2L << 30) / per));
+    }
     h->trace_slots = sd->trace_slots > 0 ? sd->trace_slots : 1024;
     h->stat_slots = std::max<long>(h->trace_slots, 65536);
-    long stride = (ws_doubles(N, sd->n_fixed, h->cmax) + 31) & ~31L;
+    long stride = std::max(ws_doubles(N, sd->n_fixed, h->cmax), ws_doubles(N, sd->n_fixed, h->cmax, true));
+    stride = (stride + 31) & ~31L;
     h->ws_stride = stride;
     h->ws_teams = std::max<long>((long)h->sms * h->blocks_per_sm, (long)h->sms * h->lat_blocks_per_sm);
+    h->ws_teams = std::max<long>(h->ws_teams, (long)h->sms * h->cr_blocks_per_sm);
     const long Sb = h->max_batch, n = 6L * N, nf = std::max(sd->n_fixed, 1), nc = std::max(sd->n_cables, 1);
     const long ts = h->trace_slots;
     rc = 0;
@@ -482,11 +507,19 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   }
   CUDA_OK(h, cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  // latency mode when the batch fits the wide teams' residency
-  const bool lat = (long)io->S <= (long)h->sms * h->lat_blocks_per_sm;
-  const int nw = lat ? h->lat_warps : h->solve_warps;
-  long blocks = std::max(1L, std::min((long)io->S, (long)h->sms * (lat ? h->lat_blocks_per_sm : h->blocks_per_sm)));
+  // latency modes: one scenario per SM (cyclic reduction) when the batch fits
+  // one wave of them, else 4-warp teams when it fits theirs; throughput mode otherwise
+  bool cr = h->cr_blocks_per_sm > 0 && (long)io->S <= (long)h->sms * h->cr_blocks_per_sm;
+  bool lat = !cr && (long)io->S <= (long)h->sms * h->lat_blocks_per_sm;
+  if (h->force_mode) {
+    cr = h->force_mode == 1 && h->cr_blocks_per_sm > 0;
+    lat = h->force_mode == 2;
+  }
+  const int nw = cr ? kCrTeamWarps : lat ? h->lat_warps : h->solve_warps;
+  const int bps = cr ? h->cr_blocks_per_sm : lat ? h->lat_blocks_per_sm : h->blocks_per_sm;
+  long blocks = std::max(1L, std::min((long)io->S, (long)h->sms * bps));
   blocks = std::min(blocks, teams_cap(h));
+  const long hot_stride = cr ? h->cr_hot_stride : h->hot_stride;
   BatchDev B;
   memset(&B, 0, sizeof(B));
   B.S = io->S;
@@ -508,8 +541,8 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   B.prof = h->prof;
   if (int rc = order_on(h, st)) return rc;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
-  CUDA_OK(h, solve_entry(nw)->launch((unsigned)blocks, (size_t)(h->hot_stride * 8), st, h->P, B, h->ws.p,
-                                                  h->ws_stride, h->hot_stride));
+  CUDA_OK(h, solve_entry(nw, cr)->launch((unsigned)blocks, (size_t)(hot_stride * 8), st, h->P, B, h->ws.p,
+                                         h->ws_stride, hot_stride));
   h->launches++;
   CUDA_OK(h, cudaGetLastError());
   return mark_done(h, st);

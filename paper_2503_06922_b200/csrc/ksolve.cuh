@@ -5,12 +5,15 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "engine.cuh"
 
 namespace accfem {
 
 struct KSolveEntry {
   int nw;
+  bool cr;             // cyclic-reduction linear algebra (latency mode: one scenario per SM)
   const void* kernel;  // for cudaFuncSetAttribute / occupancy queries
   cudaError_t (*launch)(unsigned grid, size_t smem, cudaStream_t st, const Problem& P, const BatchDev& B,
                         double* ws_base, long ws_stride, long hot_stride);
@@ -18,23 +21,29 @@ struct KSolveEntry {
 
 KSolveEntry ksolve_entry_2();
 KSolveEntry ksolve_entry_4();
+KSolveEntry ksolve_entry_cr();  // 16-warp CTA, cyclic reduction
 
 #if defined(ACCFEM_KSOLVE_NW)
 // persistent solve; one CTA of NW warps = one scenario at a time.
 // With hot_stride > 0 the team's hot arrays (factor, iterate, row state)
 // live in dynamic shared memory; otherwise everything is in the global slab.
-template <int NW>
-__global__ void __launch_bounds__(32 * NW)
+#if !defined(ACCFEM_KSOLVE_CR)
+#define ACCFEM_KSOLVE_CR 0
+#endif
+template <int NW, bool CR>
+__global__ void __launch_bounds__(32 * NW, 1)
     k_solve(Problem P, BatchDev B, double* ws_base, long ws_stride, long hot_stride) {
   extern __shared__ double smem[];
   __shared__ double red[NW];
   __shared__ int ired[NW + 1];
   __shared__ int next;
   __shared__ unsigned long long prof_acc[PF_COUNT];  // phase counters accumulate in shared memory
-  TeamCta team{TeamWarp{(int)(threadIdx.x & 31)}, (int)(threadIdx.x >> 5), NW, red, ired};
+  const TeamCta cta{TeamWarp{(int)(threadIdx.x & 31)}, (int)(threadIdx.x >> 5), NW, red, ired};
+  using Team = typename std::conditional<CR, TeamCR, TeamCta>::type;
+  const Team team(cta);
   const long wid = blockIdx.x;
   double* hot = hot_stride > 0 ? smem : nullptr;
-  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish, nullptr, nullptr, CR);
   if (threadIdx.x < PF_COUNT) prof_acc[threadIdx.x] = 0;
   ws.prof = B.prof ? prof_acc : nullptr;
   __syncthreads();
@@ -50,16 +59,22 @@ __global__ void __launch_bounds__(32 * NW)
   if (B.prof && threadIdx.x < PF_COUNT) B.prof[wid * PF_COUNT + threadIdx.x] = prof_acc[threadIdx.x];
 }
 
-template <int NW>
+template <int NW, bool CR>
 static cudaError_t ksolve_launch(unsigned grid, size_t smem, cudaStream_t st, const Problem& P, const BatchDev& B,
                                  double* ws_base, long ws_stride, long hot_stride) {
-  k_solve<NW><<<grid, 32 * NW, smem, st>>>(P, B, ws_base, ws_stride, hot_stride);
+  k_solve<NW, CR><<<grid, 32 * NW, smem, st>>>(P, B, ws_base, ws_stride, hot_stride);
   return cudaGetLastError();
 }
 #define ACCFEM_KSOLVE_PASTE2(a, b) a##b
 #define ACCFEM_KSOLVE_PASTE(a, b) ACCFEM_KSOLVE_PASTE2(a, b)
+#if ACCFEM_KSOLVE_CR
+KSolveEntry ksolve_entry_cr() {
+#else
 KSolveEntry ACCFEM_KSOLVE_PASTE(ksolve_entry_, ACCFEM_KSOLVE_NW)() {
-  return KSolveEntry{ACCFEM_KSOLVE_NW, (const void*)k_solve<ACCFEM_KSOLVE_NW>, ksolve_launch<ACCFEM_KSOLVE_NW>};
+#endif
+  constexpr bool cr = ACCFEM_KSOLVE_CR != 0;
+  return KSolveEntry{ACCFEM_KSOLVE_NW, cr, (const void*)k_solve<ACCFEM_KSOLVE_NW, cr>,
+                     ksolve_launch<ACCFEM_KSOLVE_NW, cr>};
 }
 #endif
 

@@ -92,8 +92,10 @@ constexpr int kMultiRhs = 16;  // right-hand sides solved concurrently by one wa
 // factor, the scaled iterate and the row state) come from `hot` (shared
 // memory on the device) when given, else from the global slab `base`.
 // Either base may be null to measure: *used / *hot_used receive the sizes.
+// `cr`: the coupling blocks of the factor are the cyclic-reduction layout of
+// cr.cuh (one 2N x 36 array LR, HU = LR + 36) instead of the twisted one.
 HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long* used = nullptr,
-                 long* hot_used = nullptr) {
+                 long* hot_used = nullptr, bool cr = false) {
   long n = 6L * N, E = N - 1, m = (long)nf + N;  // rows: selector rows + at most one contact per node
   long cp = cmax_polish;
   Ws w;
@@ -106,7 +108,13 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
     return r;
   };
   // hot: the factor (packed symmetric diagonal blocks, full couplings) and the solve vectors
-  w.HD = takeh(22L * N); w.HU = takeh(36 * E);
+  w.HD = takeh(22L * N);
+  if (cr) {
+    double* lr = takeh(72L * N);
+    w.HU = lr ? lr + 36 : nullptr;
+  } else {
+    w.HU = takeh(36 * E);
+  }
   w.rhs = takeh(n); w.tmp = takeh(n); w.xs = takeh(n); w.gs = takeh(n);
   w.z = takeh(m); w.y = takeh(m); w.rho = takeh(m); w.ls = takeh(m); w.us = takeh(m); w.as = takeh(3 * m);
   w.xt = w.rhs;  // the solve writes its result over the right-hand side
@@ -139,17 +147,17 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   return w;
 }
 
-HDEV long ws_doubles(int N, int nf, int cmax_polish) {
+HDEV long ws_doubles(int N, int nf, int cmax_polish, bool cr = false) {
   long used = 0;
-  ws_carve(nullptr, nullptr, N, nf, cmax_polish, &used);
+  ws_carve(nullptr, nullptr, N, nf, cmax_polish, &used, nullptr, cr);
   return used;
 }
 
 // hot-region size (doubles) of one team
-HDEV long ws_hot_doubles(int N, int nf) {
+HDEV long ws_hot_doubles(int N, int nf, bool cr = false) {
   long n = 6L * N, m = (long)nf + N;
   auto r2 = [](long k) { return (k + 1) & ~1L; };
-  return r2(22L * N) + r2(36L * (N - 1)) + 4 * r2(n) + 5 * r2(m) + r2(3 * m);
+  return r2(22L * N) + (cr ? r2(72L * N) : r2(36L * (N - 1))) + 4 * r2(n) + 5 * r2(m) + r2(3 * m);
 }
 
 // ---------------------------------------------------------------------------

@@ -15,6 +15,7 @@
 // the direct and polish solves eliminate the selector rows exactly and
 // handle the active contacts through a dense Schur complement.
 #pragma once
+#include "cr.cuh"
 #include "linalg.cuh"
 #include "mech.cuh"
 
@@ -490,6 +491,11 @@ DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
     team.sync();
   }
   return true;
+}
+#endif
+#if defined(__CUDACC__)
+DEV bool dense_chol(const TeamCR& team, int na, double* S, double* col) {
+  return dense_chol(static_cast<const TeamCta&>(team), na, S, col);
 }
 #endif
 template <class Team>

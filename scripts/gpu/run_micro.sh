@@ -1,0 +1,2 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+./scripts/micro/nd_bench > gpurun_out/nd.log 2>&1

@@ -174,6 +174,26 @@ def test_single_scenario_api_raises_reference_exception_classes():
                        x0=Configuration(w.x0[0].copy()), tol=w.tol, max_frames=w.max_frames)
 
 
+@pytest.mark.parametrize("mode", ["cr", "team4", "team2"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg2", "cfg4"])
+def test_every_kernel_mode_matches_reference_goldens(golden, name, mode, monkeypatch):
+    """The three k_solve variants -- latency mode (one 16-warp CTA per scenario,
+    cyclic reduction), 4-warp teams and 2-warp throughput teams (twisted LDL^T)
+    -- forced for any batch size, each against the reference goldens with
+    per-frame ADMM iteration counts."""
+    monkeypatch.setenv("ACCFEM_MODE", mode)
+    g = golden("solves.npz")
+    if name == "cfg1":
+        w = scenarios.cfg1(3, seed=1)
+    elif name == "cfg4":
+        w = scenarios.cfg4(16)
+    else:
+        w = scenarios.CONFIGS[name](1)
+    r, _ = device_solve(w)
+    for i in range(w.size):
+        check_against_golden(g, f"{name}_{i}", r, i)
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg4"])
 def test_global_workspace_mode_matches_reference_goldens(golden, name, monkeypatch):
     """The global-workspace mode (hot set beyond shared memory, e.g. cfg5) forced on the
