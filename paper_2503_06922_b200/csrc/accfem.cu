@@ -145,6 +145,7 @@ struct accfem_handle {
   int cr_blocks_per_sm = 0;  // the cyclic-reduction latency kernel (0: disabled)
   long cr_hot_stride = 0;
   int force_mode = 0;        // test hook ACCFEM_MODE: 1 cr, 2 4-warp teams, 3 2-warp teams (0: by batch size)
+  int hot_rows = 0;          // team kernels: lean hot set with this row capacity (0: full layout)
   int launches = 0;
   std::string err;
   Problem P;
@@ -373,16 +374,43 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
   // launch mode: hot arrays in shared memory when they fit; team width from
   // ACCFEM_TEAM_WARPS (development override) or the default
   {
-    long hot = ws_hot_doubles(N, sd->n_fixed);
-    hot = (hot + 15) & ~15L;
-    int max_smem = 0;
+    int max_smem = 0, smem_sm = 0, resv = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, device);
     const char* force_global = getenv("ACCFEM_GLOBAL_WORKSPACE");
     const char* tw = getenv("ACCFEM_TEAM_WARPS");
+    const char* lean_env = getenv("ACCFEM_LEAN");
     h->solve_warps = kTeamWarps;
     h->lat_warps = kLatencyTeamWarps;
     if (tw && solve_entry(atoi(tw))) h->solve_warps = h->lat_warps = atoi(tw);
+    // hot set of the team kernels: the full layout, or -- when it buys one more
+    // team per SM -- the lean one (factor, rhs and the row state of frames of
+    // up to `mh` rows in shared memory)
+    long hot = (ws_hot_doubles(N, sd->n_fixed) + 15) & ~15L;
+    {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, solve_entry(h->solve_warps)->kernel);
+      auto per_sm = [&](long d) { return smem_sm / (long)(d * 8 + (long)fa.sharedSizeBytes + resv); };
+      const int mfull = sd->n_fixed + N;
+      if (lean_env && lean_env[0] == '1' && hot * 8 <= max_smem) {  // opt-in: measured slower
+        const long want = per_sm(hot) + 1;
+        int best = 0;
+        for (int mh = mfull - 1; mh >= sd->n_fixed + 8 && mh > 0; --mh) {
+          const long d = (ws_hot_doubles(N, sd->n_fixed, false, mh) + 15) & ~15L;
+          if (per_sm(d) >= want) {
+            best = mh;
+            break;
+          }
+        }
+        if (best > 0) {
+          h->hot_rows = best;
+          hot = (ws_hot_doubles(N, sd->n_fixed, false, best) + 15) & ~15L;
+        }
+      }
+    }
     const bool in_smem = hot * 8 <= max_smem && !(force_global && force_global[0] == '1');
+    if (!in_smem) h->hot_rows = 0;
     h->hot_stride = in_smem ? hot : 0;
     for (int mode = 0; mode < 2; ++mode) {
       const int nw = mode ? h->lat_warps : h->solve_warps;
@@ -418,7 +446,8 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
     }
     h->trace_slots = sd->trace_slots > 0 ? sd->trace_slots : 1024;
     h->stat_slots = std::max<long>(h->trace_slots, 65536);
-    long stride = std::max(ws_doubles(N, sd->n_fixed, h->cmax), ws_doubles(N, sd->n_fixed, h->cmax, true));
+    long stride = std::max(ws_doubles(N, sd->n_fixed, h->cmax, false, h->hot_rows),
+                           ws_doubles(N, sd->n_fixed, h->cmax, true));
     stride = (stride + 31) & ~31L;
     h->ws_stride = stride;
     h->ws_teams = std::max<long>((long)h->sms * h->blocks_per_sm, (long)h->sms * h->lat_blocks_per_sm);
@@ -538,6 +567,7 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
     return fail(h, ACCFEM_E_ARG, "trace contact buffers must be given together");
   B.max_frames = io->max_frames; B.stop_on_tol = io->stop_on_tol; B.tol = io->tol;
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
+  B.hot_rows = cr ? 0 : h->hot_rows;
   B.prof = h->prof;
   if (int rc = order_on(h, st)) return rc;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));

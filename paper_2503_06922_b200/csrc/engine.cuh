@@ -43,6 +43,7 @@ struct BatchDev {
   double tol;
   int fail_on_limit;         // 1: exhausting max_frames is ST_ENGINE_MAX_FRAMES
   int cmax_polish;
+  int hot_rows;              // lean hot set: row-state capacity in shared memory (0: full layout)
   int* work_counter;         // dynamic scenario queue
   unsigned long long* prof;  // per-team phase counters (profile builds)
 };
@@ -79,6 +80,7 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
     team.sync();
   }
   F.m = F.nf + F.nc;
+  ws_rows(ws, F.m);
   external_force(team, P, tensions, applied, ws);
   build_rows(team, P, x, insertion, 1.0, F, ws);
   QpResult res;

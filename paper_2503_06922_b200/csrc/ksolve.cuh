@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
   const Team team(cta);
   const long wid = blockIdx.x;
   double* hot = hot_stride > 0 ? smem : nullptr;
-  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish, nullptr, nullptr, CR);
+  Ws ws = ws_carve(ws_base + wid * ws_stride, hot, P.m.N, P.m.n_fixed, B.cmax_polish, nullptr, nullptr, CR,
+                   hot ? B.hot_rows : 0);
   if (threadIdx.x < PF_COUNT) prof_acc[threadIdx.x] = 0;
   ws.prof = B.prof ? prof_acc : nullptr;
   __syncthreads();

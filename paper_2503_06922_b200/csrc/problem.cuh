@@ -84,7 +84,19 @@ struct Ws {
   int *act, *alist;
   unsigned long long* prof;  // PF_COUNT counters (profile builds) or null
   bool sh;                   // hot arrays live in shared memory
+  // row-state storage (z, y, rho, ls, us: cap each; as: 3 cap): `rows_hot`
+  // holds frames of at most `mh` rows, larger frames use `rows_cold` (full capacity)
+  double *rows_hot, *rows_cold;
+  int mh, mfull;
 };
+
+// point the row-state arrays at the block that holds a frame of m rows
+HDEV void ws_rows(Ws& w, int m) {
+  const bool hot = m <= w.mh;
+  double* b = hot ? w.rows_hot : w.rows_cold;
+  const long cap = hot ? w.mh : w.mfull;
+  w.z = b; w.y = b + cap; w.rho = b + 2 * cap; w.ls = b + 3 * cap; w.us = b + 4 * cap; w.as = b + 5 * cap;
+}
 
 constexpr int kMultiRhs = 16;  // right-hand sides solved concurrently by one warp (2 lanes each)
 
@@ -94,8 +106,12 @@ constexpr int kMultiRhs = 16;  // right-hand sides solved concurrently by one wa
 // Either base may be null to measure: *used / *hot_used receive the sizes.
 // `cr`: the coupling blocks of the factor are the cyclic-reduction layout of
 // cr.cuh (one 2N x 36 array LR, HU = LR + 36) instead of the twisted one.
+// `mh` > 0 selects the lean hot set of the team kernels (four teams per SM):
+// only the factor, the right-hand side and the row state of frames with at
+// most mh rows are hot; the iterate x, g_s and the sweep scratch (unused by
+// the odd-N solve) move to the slab.
 HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long* used = nullptr,
-                 long* hot_used = nullptr, bool cr = false) {
+                 long* hot_used = nullptr, bool cr = false, int mh = 0) {
   long n = 6L * N, E = N - 1, m = (long)nf + N;  // rows: selector rows + at most one contact per node
   long cp = cmax_polish;
   Ws w;
@@ -115,8 +131,23 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   } else {
     w.HU = takeh(36 * E);
   }
-  w.rhs = takeh(n); w.tmp = takeh(n); w.xs = takeh(n); w.gs = takeh(n);
-  w.z = takeh(m); w.y = takeh(m); w.rho = takeh(m); w.ls = takeh(m); w.us = takeh(m); w.as = takeh(3 * m);
+  const bool lean = mh > 0 && !cr && mh < m;
+  w.rhs = takeh(n);
+  if (lean) {
+    w.tmp = (N & 1) ? take(n) : takeh(n);
+    w.xs = take(n);
+    w.gs = take(n);
+    w.rows_hot = takeh(8L * mh);
+    w.rows_cold = take(8L * m);
+    w.mh = mh;
+  } else {
+    w.tmp = takeh(n); w.xs = takeh(n); w.gs = takeh(n);
+    w.rows_hot = takeh(8L * m);
+    w.rows_cold = w.rows_hot;
+    w.mh = (int)m;
+  }
+  w.mfull = (int)m;
+  ws_rows(w, 0);
   w.xt = w.rhs;  // the solve writes its result over the right-hand side
   // cold
   w.yprev = take(m); w.tr = take(m);
@@ -147,17 +178,19 @@ HDEV Ws ws_carve(double* base, double* hot, int N, int nf, int cmax_polish, long
   return w;
 }
 
-HDEV long ws_doubles(int N, int nf, int cmax_polish, bool cr = false) {
+HDEV long ws_doubles(int N, int nf, int cmax_polish, bool cr = false, int mh = 0) {
   long used = 0;
-  ws_carve(nullptr, nullptr, N, nf, cmax_polish, &used, nullptr, cr);
+  ws_carve(nullptr, nullptr, N, nf, cmax_polish, &used, nullptr, cr, mh);
   return used;
 }
 
-// hot-region size (doubles) of one team
-HDEV long ws_hot_doubles(int N, int nf, bool cr = false) {
+// hot-region size (doubles) of one team (ws_carve's takeh sequence)
+HDEV long ws_hot_doubles(int N, int nf, bool cr = false, int mh = 0) {
   long n = 6L * N, m = (long)nf + N;
   auto r2 = [](long k) { return (k + 1) & ~1L; };
-  return r2(22L * N) + (cr ? r2(72L * N) : r2(36L * (N - 1))) + 4 * r2(n) + 5 * r2(m) + r2(3 * m);
+  const long fac = r2(22L * N) + (cr ? r2(72L * N) : r2(36L * (N - 1)));
+  if (mh > 0 && !cr && mh < m) return fac + r2(n) + ((N & 1) ? 0 : r2(n)) + r2(8L * mh);
+  return fac + 4 * r2(n) + r2(8L * m);
 }
 
 // ---------------------------------------------------------------------------
