@@ -100,7 +100,14 @@ typedef struct {
                                      batches are processed in chunks */
   int32_t trace_slots;            /* host-path per-frame coords/contact trace staging, in
                                      scenario-frames (0: 1024) */
+  /* frame solver (SolverSettings.backend, solver.py:717-741) */
+  int32_t backend;                /* ACCFEM_BACKEND_QP or ACCFEM_BACKEND_PGS */
+  double pgs_tol;                 /* solver.py:57 */
+  int32_t pgs_min_sweep_factor;   /* solver.py:58 */
 } accfem_settings;
+
+#define ACCFEM_BACKEND_QP 0       /* accelerated_qp: Ruiz-scaled ADMM + polish (solver.py:250-528) */
+#define ACCFEM_BACKEND_PGS 1      /* pgs_baseline: projected Gauss-Seidel on the Delassus operator (solver.py:531-665) */
 
 typedef struct {
   int32_t S;                    /* scenarios in this call */

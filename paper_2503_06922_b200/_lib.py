@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, "libaccfem.so")
 c_int32, c_double, c_void_p = ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
 TRACE_STATS = 12
+BACKENDS = {"accelerated_qp": 0, "pgs_baseline": 1}  # include/accfem.h ACCFEM_BACKEND_*
 E_CODES = {100: "bad argument", 101: "CUDA error", 102: "mesh error", 103: "domain error"}
 
 
@@ -40,7 +41,8 @@ class SettingsDesc(ctypes.Structure):
                 ("sigma", c_double), ("alpha", c_double), ("beta0", c_double), ("max_iterations", c_int32),
                 ("check_interval", c_int32), ("adaptive_rho", c_int32), ("scaling_iterations", c_int32),
                 ("polish", c_int32), ("polish_capacity", c_int32), ("max_batch", c_int32),
-                ("trace_slots", c_int32)]
+                ("trace_slots", c_int32), ("backend", c_int32), ("pgs_tol", c_double),
+                ("pgs_min_sweep_factor", c_int32)]
 
 
 BATCH_FIELDS = [
@@ -148,4 +150,5 @@ class Descriptors:
                                      1 if uniform_load is not None else 0, uni, float(margin), s.eps_abs, s.eps_rel,
                                      s.rho, s.sigma, s.alpha, s.beta0, s.max_iterations, s.check_interval,
                                      1 if s.adaptive_rho else 0, s.scaling_iterations, 1 if s.polish else 0,
-                                     int(polish_capacity), int(max_batch), int(trace_slots))
+                                     int(polish_capacity), int(max_batch), int(trace_slots),
+                                     BACKENDS[s.backend], float(s.pgs_tol), int(s.pgs_min_sweep_factor))

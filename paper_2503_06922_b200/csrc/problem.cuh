@@ -20,6 +20,9 @@ struct Settings {
   double eps_abs, eps_rel, rho, sigma, alpha, beta0;
   double margin, radius;  // radius = max(margin + beta0, margin)   (engine.py:148-150, contact.py:65)
   int max_iterations, check_interval, adaptive_rho, scaling_iterations, polish;
+  int backend;                // 0 accelerated_qp, 1 pgs_baseline (solver.py:717-741)
+  double pgs_tol;             // solver.py:57
+  int pgs_min_sweep_factor;   // solver.py:58
 };
 
 struct ModelDev {

@@ -466,36 +466,59 @@ DEV bool dense_chol(const Team& team, int na, double* S) {
 }
 
 #if defined(__CUDACC__)
-// CTA version: the scaled column k is also copied to the contiguous `col`,
-// and the trailing lower triangle is updated one row per warp with the lanes
-// along the row (coalesced; the generic version walks rem^2 items with the
-// column strided through memory).  Same operations per entry.
-DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
+// CTA teams: the small dense Schur factorisation and its solves run on warp 0
+// with warp barriers only (a CTA barrier per pivot costs ~10x a pivot's work);
+// every entry sees the same sequence of operations as the generic version.
+DEV bool dense_chol_warp(const TeamWarp& w, int na, double* S) {
   for (int k = 0; k < na; ++k) {
-    double piv = S[k * na + k];
+    const double piv = S[k * na + k];
     if (!(piv > 0.0)) return false;
-    double l = sqrt(piv);
-    team.sync();
-    PARFOR(i, na - k) {
-      const int r = k + i;
-      const double v = (r == k) ? l : S[r * na + k] / l;
-      S[r * na + k] = v;
-      col[r] = v;
-    }
-    team.sync();
-    for (int r = k + 1 + team.warp; r < na; r += team.nw) {
-      const double cr = col[r];
+    const double l = sqrt(piv);
+    __syncwarp();
+    for (int r = k + w.lane; r < na; r += 32) S[r * na + k] = (r == k) ? l : S[r * na + k] / l;
+    __syncwarp();
+    for (int r = k + 1 + w.lane; r < na; r += 32) {
+      const double srk = S[r * na + k];
       double* Sr = S + (long)r * na;
-      for (int cc = k + 1 + team.w.lane; cc <= r; cc += 32) Sr[cc] -= cr * col[cc];
+      for (int cc = k + 1; cc <= r; ++cc) Sr[cc] -= srk * S[cc * na + k];
     }
-    team.sync();
+    __syncwarp();
   }
   return true;
 }
-#endif
-#if defined(__CUDACC__)
+DEV void dense_solve_warp(const TeamWarp& w, int na, const double* S, double* b) {
+  for (int k = 0; k < na; ++k) {
+    const double bk = b[k] / S[k * na + k];
+    __syncwarp();
+    if (w.lane == 0) b[k] = bk;
+    for (int r = k + 1 + w.lane; r < na; r += 32) b[r] -= S[r * na + k] * bk;
+    __syncwarp();
+  }
+  for (int k = na - 1; k >= 0; --k) {
+    const double bk = b[k] / S[k * na + k];
+    __syncwarp();
+    if (w.lane == 0) b[k] = bk;
+    for (int i = w.lane; i < k; i += 32) b[i] -= S[k * na + i] * bk;
+    __syncwarp();
+  }
+}
+DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
+  (void)col;
+  team.sync();  // S assembled by the whole team
+  return team.on_warp0([&](const TeamWarp& w) { return dense_chol_warp(w, na, S) ? 1 : 0; }) != 0;
+}
+DEV void dense_solve(const TeamCta& team, int na, const double* S, double* b) {
+  team.sync();
+  team.on_warp0([&](const TeamWarp& w) {
+    dense_solve_warp(w, na, S, b);
+    return 0;
+  });
+}
 DEV bool dense_chol(const TeamCR& team, int na, double* S, double* col) {
   return dense_chol(static_cast<const TeamCta&>(team), na, S, col);
+}
+DEV void dense_solve(const TeamCR& team, int na, const double* S, double* b) {
+  dense_solve(static_cast<const TeamCta&>(team), na, S, b);
 }
 #endif
 template <class Team>
@@ -708,6 +731,183 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
   return ST_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// projected Gauss-Seidel baseline (solve_pgs, solver.py:531-665) for the
+// selector-only constraint sets of the engine (every fixed row is a plain
+// DOF selector, so the reference's general equality rows are empty).  The
+// selector DOFs are eliminated exactly (the reduced factor with identity
+// rows), W = C~ K_ff^{-1} C~^T is formed from the multi-RHS solves
+// W_c = K_ff^{-1} C~_c (C~: contact rows with the selector DOFs zeroed) and
+// the sweeps run on one warp (lanes over the row's entries, a fixed-order
+// butterfly sum): s_i = q0_i - W_i y, y_i += s_i / W_ii, y_i >= 0.
+// ---------------------------------------------------------------------------
+#if defined(__CUDACC__)
+// one warp's fixed-order sum (every lane gets it)
+DEV double pgs_wsum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+#endif
+
+// s = q0 - W y over all rows; returns the reference's residual
+// max(max(s, 0), |y o s|_inf / max(1, |y|_inf)) (solver.py:574-582)
+template <class Team>
+DEV double pgs_residual(const Team& team, int nc, const double* W, const double* q0, const double* y) {
+  double pos = 0.0, ys = 0.0, ym = 0.0;
+  PARFOR(i, nc) {
+    double acc = 0.0;
+    for (int j = 0; j < nc; ++j) acc += W[(long)i * nc + j] * y[j];
+    const double si = q0[i] - acc;
+    pos = fmax(pos, si);
+    ys = fmax(ys, fabs(y[i] * si));
+    ym = fmax(ym, fabs(y[i]));
+  }
+  pos = team.max(pos);
+  ys = team.max(ys);
+  ym = team.max(ym);
+  return fmax(pos, ys / fmax(1.0, ym));
+}
+
+// the Gauss-Seidel sweeps; returns the sweeps run, *conv the convergence flag
+template <class Team>
+DEV int pgs_sweeps(const Team& team, int nc, const double* W, const double* q0, const double* diag, double* y,
+                   double target, int min_sweeps, int max_sweeps, bool* conv) {
+  int sweeps = 0;
+  *conv = false;
+  for (int sweep = 1; sweep <= max_sweeps; ++sweep) {
+#if defined(__CUDA_ARCH__)
+    if (team.rank() < 32) {
+      const int lane = team.rank();
+      for (int i = 0; i < nc; ++i) {
+        const double* Wi = W + (long)i * nc;
+        double acc = 0.0;
+        for (int j = lane; j < nc; j += 32) acc += Wi[j] * y[j];
+        acc = pgs_wsum(acc);
+        const double di = diag[i];
+        if (di > 0.0) {  // dead rows (W_ii <= 1e-30) keep their multiplier
+          double yi = y[i] + (q0[i] - acc) / di;
+          if (yi < 0.0) yi = 0.0;
+          __syncwarp();
+          if (lane == 0) y[i] = yi;
+        }
+        __syncwarp();
+      }
+    }
+#else
+    for (int i = 0; i < nc; ++i) {
+      const double* Wi = W + (long)i * nc;
+      double acc = 0.0;
+      for (int j = 0; j < nc; ++j) acc += Wi[j] * y[j];
+      if (diag[i] > 0.0) {
+        double yi = y[i] + (q0[i] - acc) / diag[i];
+        y[i] = yi < 0.0 ? 0.0 : yi;
+      }
+    }
+#endif
+    team.sync();
+    sweeps = sweep;
+    if (sweep >= min_sweeps && pgs_residual(team, nc, W, q0, y) <= target) {
+      *conv = true;
+      break;
+    }
+  }
+  return sweeps;
+}
+
+template <class Team>
+DEV int solve_pgs(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
+  const int N = P.m.N, n = 6 * N, nf = F.nf, nc = F.nc;
+  const int* frd = P.m.fixed_row_of_dof;
+  if (nc > cmax) return ST_CAPACITY;
+  // K_ff with the selector DOFs as identity rows; v = the eliminated free solution
+  if (reduced_factor(team, P, 0.0, ws) >= 0) return ST_LINALG;
+  eliminated_rhs(team, P, F, ws, ws.xt);
+  twisted_solve(team, N, ws.HD, ws.HU, ws.xt, ws.tmp, ws.v, 1, 0, ws.sh);
+  team.sync();
+  int sweeps = 0;
+  bool conv = true;
+  double* y = ws.Sy + cmax;    // multipliers
+  double* diag = ws.Sy;        // W_ii (dead rows: 0)
+  double* q0 = ws.Cv;
+  if (nc > 0) {
+    // W_c = K_ff^{-1} C~_c for every contact (as the polish does)
+    parfor4(team, nc * n, [&](int t) { ws.W[t] = 0.0; });
+    team.sync();
+    PARFOR(c, nc) {
+      const int nd = ws.cnode[c];
+      for (int a = 0; a < 3; ++a) {
+        const int j = 6 * nd + a;
+        if (frd[j] < 0) ws.W[(long)c * n + j] = ws.cnrm[3 * c + a];
+      }
+    }
+    team.sync();
+    twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, nc, n);
+    // Delassus W_pq = C~_p W_q, q0 = C~ v - b_adj (b_adj removes the selector DOFs' prescribed part)
+    PARFOR(t, nc * nc) {
+      const int p = t / nc, q = t - p * nc;
+      const int j0 = 6 * ws.cnode[p];
+      const double* nr = ws.cnrm + 3 * p;
+      const double* wq = ws.W + (long)q * n + j0;
+      double acc = 0.0;
+      for (int a = 0; a < 3; ++a)
+        if (frd[j0 + a] < 0) acc += nr[a] * wq[a];
+      ws.Sf[t] = acc;
+    }
+    PARFOR(c, nc) {
+      const int j0 = 6 * ws.cnode[c];
+      const double* nr = ws.cnrm + 3 * c;
+      double cv = 0.0, adj = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        const int fr = frd[j0 + a];
+        if (fr < 0) cv += nr[a] * ws.v[j0 + a];
+        else adj += nr[a] * ws.up[fr];
+      }
+      q0[c] = cv - (ws.up[nf + c] - adj);
+      y[c] = fmax(ws.warm[ws.cnode[c]], 0.0);
+      ws.alist[c] = c;  // dense_combine over every contact
+    }
+    team.sync();
+    PARFOR(c, nc) {
+      const double d = ws.Sf[(long)c * nc + c];
+      diag[c] = d <= 1e-30 ? 0.0 : d;
+    }
+    double qmax = 0.0;
+    PARFOR(c, nc) qmax = fmax(qmax, fabs(q0[c]));
+    qmax = team.max(qmax);
+    const double target = P.s.pgs_tol * fmax(qmax, 1e-12);
+    const int min_sweeps = P.s.pgs_min_sweep_factor * (nc > 1 ? nc : 1);
+    int max_sweeps = P.s.max_iterations > 250 * nc ? P.s.max_iterations : 250 * nc;
+    if (min_sweeps > max_sweeps) max_sweeps = min_sweeps;
+    sweeps = pgs_sweeps(team, nc, ws.Sf, q0, diag, y, target, min_sweeps, max_sweeps, &conv);
+    // dx = v - K_ff^{-1} C~^T y = v - sum_c y_c W_c
+    dense_combine(team, n, nc, ws.alist, ws.W, y, ws.v, ws.dx);
+  } else {
+    PARFOR(j, n) ws.dx[j] = ws.v[j];
+    team.sync();
+  }
+  // multipliers by row: contacts clamped, selectors from the equilibrium residual
+  PARFOR(c, nc) ws.yfull[nf + c] = fmax(y[c], 0.0);
+  team.sync();
+  selector_multipliers(team, P, F, ws, ws.dx, ws.yfull);
+  double pri = 0.0;
+  PARFOR(r, F.m) {
+    const double v = row_dot(P, F, ws, r, ws.dx) - ws.up[r];
+    pri = fmax(pri, r < nf ? fabs(v) : fmax(v, 0.0));
+  }
+  block_matvec(team, N, ws.KD, ws.KU, ws.dx, ws.tmp);
+  at_y(team, P, F, ws, ws.yfull, ws.w);
+  double dua = 0.0;
+  parfor4(team, n, [&](int j) { dua = fmax(dua, fabs(ws.tmp[j] + ws.g[j] + ws.w[j])); });
+  res.pri = team.max(pri);
+  res.dua = team.max(dua);
+  res.iterations = sweeps;
+  res.converged = conv ? 1 : 0;
+  res.rho_est = -1.0;
+  return conv ? ST_OK : ST_NONCONV;
+}
+
 // ---------------------------------------------------------------------------
 // one QP solve (solver.py:250-385 via solve_step 717-741).  Warm start y0 is
 // taken from ws.warm (by node) and ws.wfix.  On return ws.dx, ws.yfull.
@@ -717,6 +917,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
                  QpResult& res, int cmax) {
   const Settings& S = P.s;
   const int N = P.m.N, n = 6 * N, nf = F.nf, m = F.m;
+  if (S.backend == 1) return solve_pgs(team, P, F, ws, res, cmax);  // solve_step dispatch (solver.py:729-731)
   if (F.nc == 0) {
     PROF_T0(t_dir);
     int st = direct_solve(team, P, F, ws, res);

@@ -88,8 +88,8 @@ class Engine:
         self.cables = list(cables)
         self.fixed_specs = list(fixed_specs)
         self.settings = settings if settings is not None else SolverSettings()
-        if self.settings.backend != "accelerated_qp":
-            raise DomainError("the device path implements the accelerated_qp backend only")
+        if self.settings.backend not in ("accelerated_qp", "pgs_baseline"):
+            raise DomainError("the device path implements the accelerated_qp and pgs_baseline backends")
         self.margin = float(margin)
         if self.margin < 0.0:
             raise DomainError("margin must be >= 0")

@@ -431,15 +431,16 @@ def _dedup(flat):
 # solver settings, per-frame inputs and records
 # ----------------------------------------------------------------------------
 
-BACKENDS = ("accelerated_qp",)
+BACKENDS = ("accelerated_qp", "pgs_baseline")  # the reference's active_set_oracle stays a CPU test oracle
 
 
 @dataclass
 class SolverSettings:
     """ADMM / step settings (reference solver.py:41-68).
 
-    Only the `accelerated_qp` backend exists on the device path; the PGS and
-    active-set backends of the reference are CPU test oracles.
+    The device path implements the `accelerated_qp` backend (the hot path) and
+    the `pgs_baseline` comparison backend; the reference's
+    exhaustive `active_set_oracle` remains a CPU test oracle.
     """
 
     eps_abs: float = 1e-6

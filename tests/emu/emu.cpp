@@ -40,6 +40,7 @@ extern "C" EmuHandle* emu_create(const accfem_model_desc* md, const accfem_mesh_
   S.radius = std::max(sd->margin + sd->beta0, sd->margin);
   S.max_iterations = sd->max_iterations; S.check_interval = sd->check_interval;
   S.adaptive_rho = sd->adaptive_rho; S.scaling_iterations = sd->scaling_iterations; S.polish = sd->polish;
+  S.backend = sd->backend; S.pgs_tol = sd->pgs_tol; S.pgs_min_sweep_factor = sd->pgs_min_sweep_factor;
   h->cmax = sd->polish_capacity > 0 ? sd->polish_capacity : std::min(N, 256);
   ModelDev& M = P.m;
   M.N = N; M.l0 = md->element_rest_length;

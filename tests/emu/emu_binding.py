@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libaccfem_emu.so")
 SRC = [os.path.join(HERE, "emu.cpp")] + [
     os.path.join(HERE, "..", "..", "paper_2503_06922_b200", "csrc", f)
-    for f in ("team.cuh", "so3.cuh", "problem.cuh", "mech.cuh", "linalg.cuh", "solve.cuh", "engine.cuh",
+    for f in ("team.cuh", "so3.cuh", "problem.cuh", "mech.cuh", "linalg.cuh", "cr.cuh", "solve.cuh", "engine.cuh",
               "host_build.hpp")]
 
 
@@ -98,7 +98,8 @@ class EmuEngine:
         self.L.emu_detect(self.h, S, x.ctypes.data, tri.ctypes.data, gap.ctypes.data, pt.ctypes.data)
         return tri, gap, pt
 
-    def solve(self, x0, tensions=None, applied=None, tol=1e-9, max_frames=5000, trace_cap=0):
+    def solve(self, x0, tensions=None, applied=None, tol=1e-9, max_frames=5000, trace_cap=0, stop_on_tol=True,
+              trace_coords=False):
         S, n = x0.shape
         N = n // 6
         H = dict(x0=np.ascontiguousarray(x0, np.float64),
@@ -112,6 +113,8 @@ class EmuEngine:
                  contact_point=np.zeros((S, N, 3)))
         if trace_cap:
             H["trace_stats"] = np.zeros((S, trace_cap, _lib.TRACE_STATS))
+            if trace_coords:
+                H["trace_coords"] = np.zeros((S, trace_cap, n))
         d = _lib.BatchDesc()
         d.S = S
         for name, _ in _lib.BATCH_FIELDS:
@@ -119,8 +122,8 @@ class EmuEngine:
                 setattr(d, name, H[name].ctypes.data)
         d.trace_cap = trace_cap
         d.max_frames = max_frames
-        d.stop_on_tol = 1
+        d.stop_on_tol = 1 if stop_on_tol else 0
         d.tol = tol
-        d.fail_on_limit = 1
+        d.fail_on_limit = 1 if stop_on_tol else 0
         self.L.emu_solve_batch(self.h, ctypes.byref(d))
         return H

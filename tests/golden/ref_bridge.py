@@ -40,7 +40,9 @@ def reference_engine(w):
     settings = solver.SolverSettings(eps_abs=s.eps_abs, eps_rel=s.eps_rel, max_iterations=s.max_iterations,
                                      rho=s.rho, sigma=s.sigma, alpha=s.alpha, beta0=s.beta0,
                                      check_interval=s.check_interval, adaptive_rho=s.adaptive_rho,
-                                     scaling_iterations=s.scaling_iterations, polish=s.polish)
+                                     scaling_iterations=s.scaling_iterations, polish=s.polish,
+                                     backend=s.backend, pgs_tol=s.pgs_tol,
+                                     pgs_min_sweep_factor=s.pgs_min_sweep_factor)
     return engine.Engine(model, mesh=ref_mesh, cables=cables, fixed_specs=fixed, settings=settings,
                          margin=w.margin, uniform_load=w.uniform_load)
 

@@ -90,3 +90,47 @@ def test_emulated_detection_bit_exact(golden):
         assert np.array_equal(nodes, want[:, 1].astype(int)), s
         for k, r in zip(nodes, want):
             assert tri[0, k] == int(r[2]) and gap[0, k] == r[3] and np.array_equal(pt[0, k], r[4:7])
+
+
+def _pgs(w):
+    import dataclasses
+    w.settings = dataclasses.replace(w.settings, backend="pgs_baseline")
+    return w
+
+
+def check_pgs_static(g, H):
+    """PGS run_static vs the reference (tests/golden/make_golden_pgs.py).  PGS stops
+    at pgs_tol = 1e-6, so late frames differ in the 4th digit and the frame that
+    first reaches |dx| <= 1e-9 (a slow ~1 %/frame decay) is not pinned exactly:
+    first-frame sweeps equal, per-frame sweeps of the first 50 frames equal,
+    |dx| of the first 20 frames within 1 % (later frames move by PGS stopping
+    noise, ~1e-8 m), final coords within 1e-6, frame count within 10 %."""
+    assert H["status"][0] == 0
+    f_ref = int(g["cfg3p_frames"])
+    f = int(H["frames"][0])
+    assert abs(f - f_ref) <= 0.1 * f_ref, (f, f_ref)
+    sweeps = H["trace_stats"][0, :f, 5].astype(np.int64)
+    assert np.array_equal(sweeps[:50], g["cfg3p_iterations"][:50].astype(np.int64))
+    dx, dref = H["trace_stats"][0, :20, 0], g["cfg3p_dx_norm"][:20]
+    assert np.all(np.abs(dx - dref) <= 1e-2 * dref)
+    ref = g["cfg3p_coords"]
+    assert np.abs(H["coords"][0] - ref).max() <= 1e-6 * np.abs(ref).max()
+
+
+def test_emulated_pgs_backend_matches_reference(golden):
+    g = golden("pgs.npz")
+    w = _pgs(scenarios.cfg3p(1))
+    H = EmuEngine(**w.engine_kwargs()).solve(w.x0, w.tensions, w.applied, w.tol, w.max_frames,
+                                             trace_cap=w.max_frames)
+    check_pgs_static(g, H)
+    # the criterion-6 scenes (400 nodes, 5 / 50 contacts): 4 frames of Engine.step
+    for target in (5, 50):
+        w = _pgs(scenarios.constriction(400, target, "c400"))
+        H = EmuEngine(**w.engine_kwargs()).solve(w.x0, w.tensions, w.applied, 0.0, 4, trace_cap=4,
+                                                 stop_on_tol=False, trace_coords=True)
+        tag = f"c400_{target}"
+        assert np.array_equal(H["trace_stats"][0, :, 6].astype(np.int64), g[f"{tag}_n_c"].astype(np.int64))
+        sw = H["trace_stats"][0, :, 5].astype(np.int64)
+        assert abs(int(sw[0]) - int(g[f"{tag}_sweeps"][0])) <= 0.01 * int(g[f"{tag}_sweeps"][0]) + 1, sw
+        ref = g[f"{tag}_coords"]
+        assert np.abs(H["trace_coords"][0] - ref).max() <= 1e-6 * np.abs(ref).max(), tag

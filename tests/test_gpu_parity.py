@@ -458,3 +458,43 @@ def test_detection_on_large_tube_matches_oracle(golden):
         for c in cs:
             assert tri[s, c[0]] == c[1] and gap[s, c[0]] == c[2] and np.array_equal(pt[s, c[0]], c[3])
     assert hits > 0
+
+
+def test_pgs_backend_matches_reference(golden):
+    """SolverSettings(backend="pgs_baseline") on the device (solve_pgs, solver.py:531-665)
+    against the reference's PGS: cfg3p run_static and the criterion-6 scenes (400 nodes,
+    5 / 50 contacts, 4 Engine.step frames).  Bars as tests/test_emulation.py::check_pgs_static."""
+    import dataclasses
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_emulation import check_pgs_static
+    g = golden("pgs.npz")
+
+    def pgs(w):
+        w.settings = dataclasses.replace(w.settings, backend="pgs_baseline")
+        return w
+
+    w = pgs(scenarios.cfg3p(1))
+    r, _ = device_solve(w, trace=False)
+    eng = engine_for(w)
+    res = eng.solve_static_batch(w.x0, w.tensions, w.applied, tol=w.tol, max_frames=w.max_frames, trace_frames=512)
+    H = {"status": res.status, "frames": res.frames, "trace_stats": res.trace_stats, "coords": res.coords}
+    check_pgs_static(g, H)
+    for target in (5, 50):
+        w = pgs(scenarios.constriction(400, target, "c400"))
+        eng = engine_for(w)
+        x = torch.tensor(w.x0, device=DEV)
+        app = torch.tensor(w.applied, device=DEV)
+        state = None
+        tag = f"c400_{target}"
+        for k in range(4):
+            out, stats, state = eng.step_batch(x, None, app, None, state)
+            x = out.coords
+            st = stats.cpu().numpy()[0]
+            assert int(st[6]) == int(g[f"{tag}_n_c"][k])
+            if k == 0:
+                s_ref = int(g[f"{tag}_sweeps"][0])
+                assert abs(int(st[5]) - s_ref) <= 0.01 * s_ref + 1, (int(st[5]), s_ref)
+            ref = g[f"{tag}_coords"][k]
+            assert np.abs(x.cpu().numpy()[0] - ref).max() <= 1e-6 * np.abs(ref).max(), (tag, k)

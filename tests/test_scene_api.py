@@ -40,8 +40,9 @@ def test_fixed_rows_and_duplicates():
 
 
 def test_settings_backend_and_mesh_validation():
+    assert SolverSettings(backend="pgs_baseline").backend == "pgs_baseline"  # device PGS (§8(f) rank 3)
     with pytest.raises(DomainError):
-        SolverSettings(backend="pgs_baseline")
+        SolverSettings(backend="active_set_oracle")  # CPU test oracle only
     with pytest.raises(DomainError):
         SolverSettings(alpha=2.5)
     with pytest.raises(MeshError):
