@@ -44,7 +44,10 @@ __version__ = "0.1.0"
 
 
 def __getattr__(name):
-    if name in ("Engine", "BatchResult", "run_scenario"):
+    if name in ("Engine", "BatchResult"):
         from . import engine
         return getattr(engine, name)
+    if name in ("Timeline", "Trajectory", "run_scenario", "run_trajectories", "initial_record"):
+        from . import frames
+        return getattr(frames, name)
     raise AttributeError(name)

@@ -514,12 +514,3 @@ class Engine:
                                             pt.data_ptr(), ctypes.c_void_p(st.cuda_stream)))
         return tri, gap, pt
 
-
-def run_scenario(engine, timeline_inputs, n_frames, frame_period):
-    """Frame mode over a sequence of inputs (engine.py:300-316): one step per frame."""
-    x = engine.initial_configuration()
-    records = []
-    for k in range(1, n_frames + 1):
-        x, rec = engine.step(x, timeline_inputs(k * frame_period), t=k * frame_period, frame_index=k)
-        records.append(rec)
-    return x, records
