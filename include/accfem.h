@@ -56,9 +56,9 @@ extern "C" {
 #define ACCFEM_E_MESH 102
 #define ACCFEM_E_DOMAIN 103
 
-#define ACCFEM_TRACE_STATS 12 /* dx_norm, actuation_scale, max_penetration, complementarity_worst,
+#define ACCFEM_TRACE_STATS 14 /* dx_norm, actuation_scale, max_penetration, complementarity_worst,
                                  residual, iterations, n_c, converged, retried, complementarity_ok,
-                                 primal_residual, dual_residual */
+                                 primal_residual, dual_residual, broad-phase pairs, polish rounds */
 
 typedef struct accfem_handle accfem_handle;
 
@@ -150,6 +150,11 @@ typedef struct {
   int32_t stop_on_tol;          /* 1: run_static; 0: exactly max_frames frames (Engine.step) */
   double tol;
   int32_t fail_on_limit;        /* 1: exhausting max_frames -> ACCFEM_ENGINE_MAX_FRAMES */
+  /* optional per-team (CTA) load-balance record of the launch: 4 int64 per
+     team -- scenarios solved, busy ns, start ns, end ns (%globaltimer) --
+     for up to team_stats_cap teams (accfem_last_launch_teams() were used) */
+  int64_t* team_stats;
+  int32_t team_stats_cap;
 } accfem_batch;
 
 int accfem_create(const accfem_model_desc* model, const accfem_mesh_desc* mesh, const accfem_settings* settings,
@@ -174,6 +179,7 @@ int accfem_teams_resident(accfem_handle* h);
 long long accfem_workspace_bytes(accfem_handle* h);
 int accfem_launches(accfem_handle* h); /* kernels launched by this handle so far */
 int accfem_max_batch(accfem_handle* h); /* host-path chunk size (accfem_settings.max_batch) */
+int accfem_last_launch_teams(accfem_handle* h); /* CTAs (teams) of the last solve launch */
 
 /* broad-phase grid built on the device by accfem_create (replaces the
  * AabbTree build, mesh.py:204-243): dims[3], cell count, list entries; and a

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libaccfem.so")
 
 c_int32, c_double, c_void_p = ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
-TRACE_STATS = 12
+TRACE_STATS = 14
 BACKENDS = {"accelerated_qp": 0, "pgs_baseline": 1}  # include/accfem.h ACCFEM_BACKEND_*
 E_CODES = {100: "bad argument", 101: "CUDA error", 102: "mesh error", 103: "domain error"}
 
@@ -58,6 +58,7 @@ BATCH_FIELDS = [
     ("trace_contact_node", c_void_p), ("trace_contact_triangle", c_void_p), ("trace_contact_gap", c_void_p),
     ("trace_contact_force", c_void_p), ("trace_contact_point", c_void_p),
     ("max_frames", c_int32), ("stop_on_tol", c_int32), ("tol", c_double), ("fail_on_limit", c_int32),
+    ("team_stats", c_void_p), ("team_stats_cap", c_int32),
 ]
 
 
@@ -81,6 +82,7 @@ SIGNATURES = {
     "accfem_workspace_bytes": (ctypes.c_longlong, [c_void_p]),
     "accfem_launches": (ctypes.c_int, [c_void_p]),
     "accfem_max_batch": (ctypes.c_int, [c_void_p]),
+    "accfem_last_launch_teams": (ctypes.c_int, [c_void_p]),
     "accfem_grid_shape": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "accfem_grid_download": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
 }

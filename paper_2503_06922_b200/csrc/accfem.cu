@@ -146,6 +146,7 @@ struct accfem_handle {
   long cr_hot_stride = 0;
   int force_mode = 0;        // test hook ACCFEM_MODE: 1 cr, 2 4-warp teams, 3 2-warp teams (0: by batch size)
   int hot_rows = 0;          // team kernels: lean hot set with this row capacity (0: full layout)
+  int last_teams = 0;        // CTAs of the last solve launch
   int launches = 0;
   std::string err;
   Problem P;
@@ -523,6 +524,7 @@ extern "C" int accfem_teams_resident(accfem_handle* h) { return h ? h->sms * h->
 extern "C" long long accfem_workspace_bytes(accfem_handle* h) { return h ? (long long)h->ws.n * 8 : 0; }
 extern "C" int accfem_launches(accfem_handle* h) { return h ? h->launches : 0; }
 extern "C" int accfem_max_batch(accfem_handle* h) { return h ? h->max_batch : 0; }
+extern "C" int accfem_last_launch_teams(accfem_handle* h) { return h ? h->last_teams : 0; }
 
 extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void* stream) {
   if (!h || !io) return ACCFEM_E_ARG;
@@ -569,6 +571,9 @@ extern "C" int accfem_solve_batch(accfem_handle* h, const accfem_batch* io, void
   B.max_frames = io->max_frames; B.stop_on_tol = io->stop_on_tol; B.tol = io->tol;
   B.fail_on_limit = io->fail_on_limit; B.cmax_polish = h->cmax; B.work_counter = h->counter.p;
   B.hot_rows = cr ? 0 : h->hot_rows;
+  B.team_stats = reinterpret_cast<long long*>(io->team_stats);
+  B.team_stats_cap = io->team_stats ? io->team_stats_cap : 0;
+  h->last_teams = (int)blocks;
   B.prof = h->prof;
   if (int rc = order_on(h, st)) return rc;
   CUDA_OK(h, cudaMemsetAsync(h->counter.p, 0, sizeof(int), st));
@@ -677,6 +682,8 @@ extern "C" int accfem_solve_batch_host(accfem_handle* h, const accfem_batch* io,
     d.rho_out = io->rho_out ? h->o_rho.p : nullptr;
     d.trace_stats = nullptr;
     d.trace_coords = nullptr;
+    d.team_stats = nullptr;  // device-pointer calls only
+    d.team_stats_cap = 0;
     d.trace_contact_node = nullptr;
     d.trace_contact_triangle = nullptr;
     d.trace_contact_gap = d.trace_contact_force = d.trace_contact_point = nullptr;

@@ -44,12 +44,14 @@ struct BatchDev {
   int fail_on_limit;         // 1: exhausting max_frames is ST_ENGINE_MAX_FRAMES
   int cmax_polish;
   int hot_rows;              // lean hot set: row-state capacity in shared memory (0: full layout)
+  long long* team_stats;     // 4 per team: scenarios, busy ns, start ns, end ns (or null)
+  int team_stats_cap;
   int* work_counter;         // dynamic scenario queue
   unsigned long long* prof;  // per-team phase counters (profile builds)
 };
 
-constexpr int kTraceStats = 12;  // dx_norm, act_scale, max_pen, compl_worst, residual, iterations,
-                                 // n_c, converged, retried, compl_ok, pri, dua
+constexpr int kTraceStats = 14;  // dx_norm, act_scale, max_pen, compl_worst, residual, iterations,
+                                 // n_c, converged, retried, compl_ok, pri, dua, pairs, polish_rounds
 
 // one frame.  x (6N) is advanced in place.  Returns a status.
 template <class Team>
@@ -73,7 +75,8 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
   }
   F.nf = M.n_fixed;
   PROF_T0(t_det);
-  F.nc = P.mesh.T > 0 ? detect_pass(team, P, x, ws) : 0;
+  int pairs = 0;
+  F.nc = P.mesh.T > 0 ? detect_pass(team, P, x, ws, &pairs) : 0;
   PROF_ADD(ws, PF_DETECT, t_det);
   if (P.mesh.T == 0) {
     PARFOR(k, N) ws.crow_of_node[k] = -1;
@@ -86,11 +89,13 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
   QpResult res;
   int retried = 0;
   int code = solve_qp(team, P, F, ws, rho, has_wfix, res, B.cmax_polish);
+  int rounds = res.polish_rounds;
   if (code == ST_NONCONV) {
     retried = 1;
     if (P.s.adaptive_rho && res.rho_est >= 0.0) rho = res.rho_est;
     build_rows(team, P, x, insertion * 0.5, 1.0, F, ws);
     code = solve_qp(team, P, F, ws, rho, has_wfix, res, B.cmax_polish);
+    rounds += res.polish_rounds;
     if (code == ST_NONCONV) return ST_ENGINE_SOLVER;
   }
   if (code != ST_OK) return code;
@@ -177,6 +182,8 @@ DEV int frame_step(const Team& team, const Problem& P, const BatchDev& B, int s,
   st.residual = 0.0;
   st.pri = res.pri;
   st.dua = res.dua;
+  st.pairs = pairs;
+  st.polish_rounds = rounds;
   (void)B;
   (void)s;
   return ST_OK;
@@ -217,6 +224,8 @@ DEV void write_trace(const Team& team, const BatchDev& B, int s, int f, const Fr
     t[9] = st.compl_ok;
     t[10] = st.pri;
     t[11] = st.dua;
+    t[12] = st.pairs;
+    t[13] = st.polish_rounds;
   }
 }
 

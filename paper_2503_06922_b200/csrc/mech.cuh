@@ -295,11 +295,12 @@ DEV void closest_point(const double* p, const double* a, const double* b, const 
 // per-node winner (min signed distance, ties to the lower triangle id),
 // then node-ordered compaction.  Returns the contact count.
 template <class Team>
-DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws) {
+DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws, int* pairs_out = nullptr) {
   const MeshDev& G = P.mesh;
   const int N = P.m.N;
   const double margin = P.s.margin, radius = P.s.radius;
   const double r2 = xmul(radius, radius);
+  int pairs = 0;  // (node, triangle) pairs that pass the broad phase
   PARFOR(k, N) {
     double p[3] = {x[6 * k], x[6 * k + 1], x[6 * k + 2]};
     int best_t = -1;
@@ -342,6 +343,7 @@ DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws)
           gg[a] = uu > v ? uu : v;
         }
         if (!(edot3(gg, gg) <= r2)) continue;
+        ++pairs;
         const double* cor = G.corners + 9 * t;
         double cl[3], off[3];
         closest_point(p, cor, cor + 3, cor + 6, cl);
@@ -367,6 +369,7 @@ DEV int detect_pass(const Team& team, const Problem& P, const double* x, Ws& ws)
     ws.cpp[3 * k + 1] = best_pp[1];
     ws.cpp[3 * k + 2] = best_pp[2];
   }
+  if (pairs_out) *pairs_out = team.isum(pairs);
   team.sync();
   // compaction in node order; contact c is stored at index c of the c* arrays
   // (written in place: contact index <= node index, chunks processed in order)

@@ -202,6 +202,7 @@ HDEV long ws_hot_doubles(int N, int nf, bool cr = false, int mh = 0) {
 struct FrameStats {
   double dx_norm, actuation_scale, max_penetration, compl_worst, residual, pri, dua;
   int iterations, n_c, converged, retried, compl_ok;
+  int pairs, polish_rounds;  // broad-phase pairs and polish rounds of the frame (measurement)
 };
 
 }  // namespace accfem

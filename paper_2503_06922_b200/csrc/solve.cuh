@@ -29,6 +29,7 @@ enum Status {
 struct QpResult {
   double pri, dua, rho_est;  // rho_est < 0: none reported
   int iterations, converged;
+  int polish_rounds;         // active-set rounds run by the polish
 };
 
 struct Frame {  // per-frame problem sizes
@@ -619,6 +620,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
   PROF_ADD(ws, PF_POL_W, t_pw);
   PROF_T0(t_pr);
   for (int round = 0; round < 6; ++round) {
+    res.polish_rounds = round + 1;
     // active contact list in row order
     int na = 0;
     for (int base = 0; base < nc; base += team.size()) {
@@ -917,6 +919,7 @@ DEV int solve_qp(const Team& team, const Problem& P, const Frame& F, Ws& ws, dou
                  QpResult& res, int cmax) {
   const Settings& S = P.s;
   const int N = P.m.N, n = 6 * N, nf = F.nf, m = F.m;
+  res.polish_rounds = 0;
   if (S.backend == 1) return solve_pgs(team, P, F, ws, res, cmax);  // solve_step dispatch (solver.py:729-731)
   if (F.nc == 0) {
     PROF_T0(t_dir);

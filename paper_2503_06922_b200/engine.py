@@ -350,7 +350,7 @@ class Engine:
                            contact_force=z((S, N, 3)), contact_normal=z((S, N, 3)), contact_point=z((S, N, 3)))
 
     def solve_static_batch(self, x0, tensions=None, applied=None, insertion=None, tol=1e-9, max_frames=5000,
-                           out=None, stream=None, host=None, trace_frames=0):
+                           out=None, stream=None, host=None, trace_frames=0, team_stats=None):
         """run_static of S independent scenarios, each from a fresh Engine state.
 
         Inputs are (S, 6N) / (S, n_cables) arrays: torch CUDA tensors (device
@@ -358,7 +358,10 @@ class Engine:
         call).  Status codes per scenario follow include/accfem.h.
         `trace_frames` > 0 also records the first `trace_frames` frames' stats
         of every scenario (FrameRecord fields, include/accfem.h
-        ACCFEM_TRACE_STATS layout) into `out.trace_stats` (S, trace_frames, 12).
+        ACCFEM_TRACE_STATS layout) into `out.trace_stats` (S, trace_frames, 14).
+        `team_stats` (device calls): an int64 CUDA tensor (T, 4) receiving the
+        launch's per-team load-balance record (scenarios, busy ns, start ns,
+        end ns) for the first T teams (accfem_last_launch_teams() were used).
         """
         import torch
 
@@ -402,6 +405,14 @@ class Engine:
                                               device=self.device)
             desc.trace_cap = int(trace_frames)
             desc.trace_stats = _lib.ptr(out.trace_stats)
+        if team_stats is not None and not host:
+            import torch as _t
+            if team_stats.dtype != _t.int64 or team_stats.device != self.device or team_stats.dim() != 2 \
+                    or team_stats.shape[1] != 4 or not team_stats.is_contiguous():
+                raise DomainError("team_stats must be a contiguous int64 (T, 4) tensor on the engine device")
+            desc.team_stats = _lib.ptr(team_stats)
+            desc.team_stats_cap = int(team_stats.shape[0])
+            keep.append(team_stats)
         desc.max_frames = int(max_frames)
         desc.stop_on_tol = 1
         desc.tol = float(tol)
@@ -429,7 +440,7 @@ class Engine:
         x (S, 6N), tensions (S, n_cables), applied (S, 6N), insertion (S,) are
         torch CUDA tensors; `state` carries each scenario's warm multipliers and
         rho between frames (a fresh state if None).  Returns (BatchResult with
-        the new coords and last-frame contacts, per-frame stats (S, 12) in the
+        the new coords and last-frame contacts, per-frame stats (S, 14) in the
         layout of include/accfem.h ACCFEM_TRACE_STATS, new BatchState).
         """
         import torch

@@ -29,6 +29,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _lib
 from .errors import ScenarioError, exception_for_status
 from .scene import (
     MATERIAL_PRESETS,
@@ -187,7 +188,7 @@ def run_scenario(engine, traj):
 @dataclass
 class TrajectoryBatch:
     """Outputs of run_trajectories for S trajectories of F = max frames:
-    per-frame stats (S, F, 12) in the ACCFEM_TRACE_STATS layout, coords
+    per-frame stats (S, F, 14) in the ACCFEM_TRACE_STATS layout, coords
     (S, F, 6N), contact triangle per node (S, F, N; -1 none), status (S) and the
     number of frames each trajectory completed (S)."""
 
@@ -214,7 +215,7 @@ def run_trajectories(engine, trajs, records=False):
     dev = engine.device
     x = torch.tensor(np.tile(engine.model.rest_configuration, (S, 1)), device=dev)
     state = None
-    stats = np.zeros((S, F, 12))
+    stats = np.zeros((S, F, _lib.TRACE_STATS))
     coords = np.zeros((S, F, n))
     ctri = np.full((S, F, N), -1, np.int32)
     status = np.zeros(S, np.int32)

@@ -1,6 +1,8 @@
 """Scenario sharding across ranks (one process per GPU) and the timing
 reduction bench.py uses.  The path has no data exchange: each rank solves
-its own contiguous shard; only the step time is reduced (max over ranks)."""
+its own contiguous shard (or claims chunks from a dynamic queue); only the
+step time is reduced (max over ranks) and the results gathered at the end
+(SURVEY §8(e))."""
 
 from __future__ import annotations
 
@@ -36,4 +38,39 @@ def gather_results(arrays, dist=None, device=None):
         parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
         dist.all_gather(parts, t)
         out.append(torch.cat(parts).cpu().numpy())
+    return out
+
+
+class ChunkQueue:
+    """Dynamic cross-rank work queue: chunks of `chunk` scenarios of a `total`
+    table claimed through an atomic counter in the process group's key-value
+    store (one `add` per claim), so ranks that draw cheap scenarios take more
+    chunks (frame counts vary 3-400 per scenario)."""
+
+    def __init__(self, store, key, total, chunk):
+        if chunk < 1:
+            raise ValueError("chunk must be >= 1")
+        self.store, self.key, self.total, self.chunk = store, key, int(total), int(chunk)
+
+    def next(self):
+        """[start, stop) of the next unclaimed chunk, or None when the table is exhausted."""
+        i = int(self.store.add(self.key, 1)) - 1
+        a = i * self.chunk
+        if a >= self.total:
+            return None
+        return a, min(self.total, a + self.chunk)
+
+
+def all_max(arrays, dist=None):
+    """Element-wise max over ranks of int64 arrays (ranks fill the entries they
+    solved and -1 elsewhere): the union of a dynamically chunked run."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return arrays
+    import numpy as np
+    import torch
+    out = []
+    for a in arrays:
+        t = torch.tensor(np.asarray(a, dtype=np.int64))  # a copy: the reduction is in place
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out.append(t.numpy())
     return out

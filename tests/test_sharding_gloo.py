@@ -53,3 +53,35 @@ def test_shard_range():
     assert shard_range(7, 8, 8192, 65536) == (57344, 65536)
     with pytest.raises(ValueError):
         shard_range(2, 2, 1, 10)
+
+
+def _queue_worker(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_06922_b200 import shard
+    store = dist.distributed_c10d._get_default_store()
+    total = 1000
+    mine = np.full(total, -1, np.int64)
+    q = shard.ChunkQueue(store, "t0", total, 64)
+    while True:
+        r = q.next()
+        if r is None:
+            break
+        mine[r[0]:r[1]] = rank
+    owners = shard.all_max([mine], dist)[0]
+    claimed = shard.gather_results([np.array([(mine >= 0).sum()])], dist)[0]
+    if rank == 0:
+        np.savez(out_path, owners=owners, claimed=claimed)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dynamic_chunk_queue_covers_the_table_once(tmp_path):
+    """ChunkQueue over the gloo store: every scenario claimed by exactly one rank."""
+    out = str(tmp_path / "q.npz")
+    port = 30500 + os.getpid() % 1000
+    tmp.spawn(_queue_worker, args=(2, port, out), nprocs=2, join=True)
+    r = np.load(out)
+    assert (r["owners"] >= 0).all()
+    assert int(r["claimed"].sum()) == 1000
