@@ -21,12 +21,20 @@ SRC = [os.path.join(HERE, "emu.cpp")] + [
               "host_build.hpp")]
 
 
-def build(force=False):
+SO_ASAN = os.path.join(HERE, "libaccfem_emu_asan.so")
+
+
+def build(force=False, sanitize=False):
+    """The emulation library; sanitize=True builds the AddressSanitizer +
+    UndefinedBehaviorSanitizer variant (load it with libasan preloaded)."""
+    so = SO_ASAN if sanitize else SO
     newest = max(os.path.getmtime(p) for p in SRC)
-    if force or not os.path.exists(SO) or os.path.getmtime(SO) < newest:
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-shared", "-fPIC", "-o", SO,
+    if force or not os.path.exists(so) or os.path.getmtime(so) < newest:
+        flags = ["-O1", "-g", "-fsanitize=address,undefined", "-fno-omit-frame-pointer",
+                 "-fno-sanitize-recover=undefined"] if sanitize else ["-O2"]
+        subprocess.check_call(["g++", *flags, "-std=c++17", "-ffp-contract=off", "-shared", "-fPIC", "-o", so,
                                SRC[0]])
-    return SO
+    return so
 
 
 _EMU = None
@@ -35,7 +43,7 @@ _EMU = None
 def lib():
     global _EMU
     if _EMU is None:
-        L = ctypes.CDLL(build())
+        L = ctypes.CDLL(os.environ.get("ACCFEM_EMU_SO") or build())
         L.emu_create.restype = ctypes.c_void_p
         L.emu_create.argtypes = [ctypes.POINTER(_lib.ModelDesc), ctypes.POINTER(_lib.MeshDesc),
                                  ctypes.POINTER(_lib.SettingsDesc)]
