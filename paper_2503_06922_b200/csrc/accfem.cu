@@ -9,6 +9,7 @@
 //   k_detect          unit entry point: per-node contact winner
 //   k_grid_*          broad-phase grid build over the lumen mesh (grid.cuh)
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -247,10 +248,20 @@ static cudaError_t build_grid(accfem_handle* h, const accfem_host::HostMesh& hm)
   GRID_OK(cudaMemcpy(count.p, h->cell_start.p, (ncell + 1) * sizeof(int), cudaMemcpyDeviceToDevice));
   k_grid_fill<<<tblocks, tb>>>(g, count.p, unsorted.p);
   GRID_OK(cudaGetLastError());
-  k_grid_sort<<<(int)std::min<long>((ncell + 7) / 8, 148L * 64), 256>>>(ncell, h->cell_start.p, unsorted.p,
-                                                                      h->cell_tris.p);
-  GRID_OK(cudaGetLastError());
-  h->launches += 3;
+  // order every cell's list by triangle id (the host build's order): a segmented
+  // radix sort over the cell ranges (a per-cell rank sort is quadratic in the
+  // list length, ~500 entries per cell on dense meshes)
+  {
+    size_t sort_bytes = 0;
+    GRID_OK(cub::DeviceSegmentedSort::SortKeys(nullptr, sort_bytes, unsorted.p, h->cell_tris.p, entries, (int)ncell,
+                                               h->cell_start.p, h->cell_start.p + 1));
+    DevBuf<char> sort_tmp;
+    GRID_OK(sort_tmp.alloc(std::max<size_t>(sort_bytes, 1)));
+    GRID_OK(cub::DeviceSegmentedSort::SortKeys(sort_tmp.p, sort_bytes, unsorted.p, h->cell_tris.p, entries,
+                                               (int)ncell, h->cell_start.p, h->cell_start.p + 1));
+    GRID_OK(cudaDeviceSynchronize());
+  }
+  h->launches += 2;  // k_grid_count, k_grid_fill (the scan and the sort are cub's)
   GRID_OK(cudaDeviceSynchronize());
 #undef GRID_OK
   return cudaSuccess;

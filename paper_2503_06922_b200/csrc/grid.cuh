@@ -10,7 +10,9 @@
 //                  radius of its AABB (atomicAdd per cell)
 //   scan           exclusive sum of the counts -> CSR cell_start
 //   k_grid_fill    one warp per triangle: claim a slot per cell
-//   k_grid_sort    one warp per cell: order its list by triangle id
+//   sort           cub segmented radix sort of every cell's list by triangle id
+//                  (accfem.cu; k_grid_sort, the earlier per-cell rank sort, is
+//                  kept for the microbenchmarks)
 //
 // The result equals the host build (host_build.hpp) entry for entry: the
 // cell ranges and the cell-vs-AABB distance test use the same operation
