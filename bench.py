@@ -226,21 +226,28 @@ def fp64_peak_tflops(dev):
 
 
 def library_sha():
-    from paper_2503_06922_b200 import _lib
-    with open(_lib.LIB_PATH, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()[:16]
+    """Identity of the library build: sha256 of its sources and nvcc flags
+    (build.sources(), build.FLAGS) -- the binary itself embeds nvcc temp-file
+    names, so its bytes differ between otherwise identical builds."""
+    from paper_2503_06922_b200 import build
+    h = hashlib.sha256(" ".join(build.FLAGS).encode())
+    for p in sorted(build.sources()):
+        with open(p, "rb") as fh:
+            h.update(os.path.basename(p).encode() + fh.read())
+    return h.hexdigest()[:16]
 
 
 def ncu_profile(sha):
     """DRAM bytes and FP64-pipe utilisation of k_solve per solve from the committed
     ncu capture (profiles/k_solve_ncu.json) -- used only if it was taken of this
-    very library build (same sha256 prefix), else reported as null."""
+    very library build (same source sha256 prefix, library_sha()), else reported
+    as stale."""
     p = os.path.join(ROOT, "profiles", "k_solve_ncu.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
         d = json.load(fh)
-    return d if d.get("library_sha256_16") == sha else {"stale": True, "source": d.get("source")}
+    return d if d.get("library_source_sha256_16") == sha else {"stale": True, "source": d.get("source")}
 
 
 def load_balance(ts):
@@ -481,7 +488,7 @@ def main():
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in "
                                         "MEASURED_PEAKS.json)",
                          "flop_per_solve": fl, "pairs_per_solve": pairs, "polish_rounds_per_solve": rounds,
-                         "library_sha256_16": sha,
+                         "library_source_sha256_16": sha,
                          "kernel": "k_solve<2> (persistent, one 2-warp CTA per scenario, "
                                    f"{eng._lib.accfem_teams_resident(eng._h)} resident)"},
             "load_balance": lb,
