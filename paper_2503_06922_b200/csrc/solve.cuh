@@ -503,17 +503,63 @@ DEV void dense_solve_warp(const TeamWarp& w, int na, const double* S, double* b)
     __syncwarp();
   }
 }
+// up to this many active contacts the Schur factor/solves run on one warp;
+// larger systems (the 1000-node configs: 200-250 contacts) use the whole team,
+// the scaled column copied to the contiguous `col` and the trailing lower
+// triangle updated one row per warp with the lanes along the row (coalesced)
+constexpr int kDenseWarpMax = 64;
 DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
-  (void)col;
   team.sync();  // S assembled by the whole team
-  return team.on_warp0([&](const TeamWarp& w) { return dense_chol_warp(w, na, S) ? 1 : 0; }) != 0;
+  if (na <= kDenseWarpMax)
+    return team.on_warp0([&](const TeamWarp& w) { return dense_chol_warp(w, na, S) ? 1 : 0; }) != 0;
+  for (int k = 0; k < na; ++k) {
+    double piv = S[k * na + k];
+    if (!(piv > 0.0)) return false;
+    double l = sqrt(piv);
+    team.sync();
+    PARFOR(i, na - k) {
+      const int r = k + i;
+      const double v = (r == k) ? l : S[r * na + k] / l;
+      S[r * na + k] = v;
+      col[r] = v;
+    }
+    team.sync();
+    for (int r = k + 1 + team.warp; r < na; r += team.nw) {
+      const double cr = col[r];
+      double* Sr = S + (long)r * na;
+      for (int cc = k + 1 + team.w.lane; cc <= r; cc += 32) Sr[cc] -= cr * col[cc];
+    }
+    team.sync();
+  }
+  return true;
 }
 DEV void dense_solve(const TeamCta& team, int na, const double* S, double* b) {
   team.sync();
-  team.on_warp0([&](const TeamWarp& w) {
-    dense_solve_warp(w, na, S, b);
-    return 0;
-  });
+  if (na <= kDenseWarpMax) {
+    team.on_warp0([&](const TeamWarp& w) {
+      dense_solve_warp(w, na, S, b);
+      return 0;
+    });
+    return;
+  }
+  for (int k = 0; k < na; ++k) {
+    team.sync();
+    double bk = b[k] / S[k * na + k];
+    team.sync();
+    if (team.rank() == 0) b[k] = bk;
+    PARFOR(i, na - k - 1) {
+      int r = k + 1 + i;
+      b[r] -= S[r * na + k] * bk;
+    }
+  }
+  for (int k = na - 1; k >= 0; --k) {
+    team.sync();
+    double bk = b[k] / S[k * na + k];
+    team.sync();
+    if (team.rank() == 0) b[k] = bk;
+    PARFOR(i, k) b[i] -= S[k * na + i] * bk;
+  }
+  team.sync();
 }
 DEV bool dense_chol(const TeamCR& team, int na, double* S, double* col) {
   return dense_chol(static_cast<const TeamCta&>(team), na, S, col);
