@@ -864,8 +864,9 @@ DEV int pgs_sweeps(const Team& team, int nc, const double* W, const double* q0, 
   return sweeps;
 }
 
+// not inlined: the comparison backend keeps its registers out of the hot kernel's allocation
 template <class Team>
-DEV int solve_pgs(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
+DEVNI int solve_pgs(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
   const int N = P.m.N, n = 6 * N, nf = F.nf, nc = F.nc;
   const int* frd = P.m.fixed_row_of_dof;
   if (nc > cmax) return ST_CAPACITY;
