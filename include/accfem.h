@@ -126,7 +126,7 @@ typedef struct {
   int32_t* converged;           /* S: reached |dx| <= tol */
   double* residual;             /* S equilibrium residual of the last frame */
   int32_t* n_contacts;          /* S contacts of the last frame */
-  int32_t* contact_node;        /* S x N */
+  int32_t* contact_node;        /* S x N: the first n_contacts[s] entries are defined */
   int32_t* contact_triangle;    /* S x N */
   double* contact_gap;          /* S x N */
   double* contact_multiplier;   /* S x N (step-limited) */

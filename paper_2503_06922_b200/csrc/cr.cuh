@@ -197,8 +197,12 @@ static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, 
   int so[6];
 #pragma unroll
   for (int t = 0; t < 6; ++t) so[t] = sidx(r, t);
+  // levels with at most kTail items run on warp 0 alone (warp barriers, up to
+  // three passes of its five groups) instead of a CTA barrier each: measured
+  // faster for N = 1001 (cfg5 -9 %), slower for N = 101 (+4 %)
+  const int kTail = (nrhs == 1 && N > 256) ? 15 : 5;
   int ltop = 0;
-  while (ltop < Lv && cr_surv_count(N, ltop) * nrhs > 5) ++ltop;
+  while (ltop < Lv && cr_surv_count(N, ltop) * nrhs > kTail) ++ltop;
   CR_T(0);
   for (int l = 0; l < ltop; ++l) {
     const int s = 1 << l, ns = cr_surv_count(N, l);
@@ -212,14 +216,40 @@ static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, 
     team.sync();
     CR_T(1 + l);
   }
-  if (ltop < Lv || nrhs <= 5) {
+  if (nrhs == 1) {
+    // single right-hand side: the top levels on warp 0, groups strided over the blocks
+    if (team.warp == 0 && glane) {
+      const unsigned m = 0x3fffffffu;
+      for (int l = ltop; l < Lv; ++l) {
+        const int s = 1 << l, ns = cr_surv_count(N, l);
+        for (int q = grp; q < ns; q += 5) v[6 * (2 * s * q) + r] = cr_fwd_row(N, F, v, 2 * s * q, s, r);
+        __syncwarp(m);
+      }
+      double a = 0.0;
+      if (grp == 0) a = cr_root_row(F, v, r, so);
+      __syncwarp(m);
+      if (grp == 0) v[r] = a;
+      __syncwarp(m);
+      CR_T(20);
+      for (int l = Lv - 1; l >= ltop; --l) {
+        const int s = 1 << l, ne = cr_elim_count(N, l);
+        for (int q0 = 0; q0 < ne; q0 += 5) {
+          const int q = q0 + grp, i = s + 2 * s * q;
+          if (q < ne) a = cr_bwd_row(N, F, v, i, s, r, so);
+          __syncwarp(m);
+          if (q < ne) v[6 * i + r] = a;
+          __syncwarp(m);
+        }
+      }
+    }
+  } else if (ltop < Lv || nrhs <= 5) {
     // nrhs * blocks <= 5 from here on: warp 0 alone, group -> (rhs, block)
     if (team.warp == 0 && glane) {
       const unsigned m = 0x3fffffffu;
       const int g = grp;
       for (int l = ltop; l < Lv; ++l) {
         const int s = 1 << l, ns = cr_surv_count(N, l);
-        const int gg = nrhs == 1 ? (g < ns ? 0 : 1) : g / ns, q = g - gg * ns;
+        const int gg = g / ns, q = g - gg * ns;
         if (gg < nrhs) {
           double* vg = v + gg * stride;
           vg[6 * (2 * s * q) + r] = cr_fwd_row(N, F, vg, 2 * s * q, s, r);
@@ -231,10 +261,9 @@ static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, 
       __syncwarp(m);
       if (g < nrhs) v[g * stride + r] = a;
       __syncwarp(m);
-      CR_T(20);
       for (int l = Lv - 1; l >= ltop; --l) {
         const int s = 1 << l, ne = cr_elim_count(N, l);
-        const int gg = nrhs == 1 ? (g < ne ? 0 : 1) : (ne > 0 ? g / ne : nrhs), q = g - gg * ne;
+        const int gg = ne > 0 ? g / ne : nrhs, q = g - gg * ne;
         const int i = s + 2 * s * q;
         if (gg < nrhs) a = cr_bwd_row(N, F, v + gg * stride, i, s, r, so);
         __syncwarp(m);

@@ -512,3 +512,54 @@ def test_repeated_launches_are_bit_identical(mode, monkeypatch):
     r2, _ = device_solve(w)
     for f in ("coords", "status", "frames", "contact_force", "trace_stats"):
         assert np.array_equal(getattr(r1, f), getattr(r2, f)), (mode, f)
+
+
+def test_host_path_chunks_and_cross_stream_ordering():
+    """ADVICE fixes: a host batch larger than the handle's staging (max_batch) runs in
+    chunks with the same results, and launches of one handle on two streams are
+    ordered (the second waits on the first's completion event) instead of racing on
+    the shared work queue and workspace."""
+    from paper_2503_06922_b200.engine import Engine
+    w = scenarios.cfg4(40, start=3000)
+    big = Engine(**w.engine_kwargs(), device=0)
+    small = Engine(**w.engine_kwargs(), device=0, max_batch=7)
+    assert small._lib.accfem_max_batch(small._h) == 7
+    rb = big.solve_static_batch(w.x0, w.tensions, w.applied, tol=w.tol, max_frames=w.max_frames)
+    rs = small.solve_static_batch(w.x0, w.tensions, w.applied, tol=w.tol, max_frames=w.max_frames)
+    for f in ("coords", "status", "frames", "n_contacts"):
+        assert np.array_equal(getattr(rb, f), getattr(rs, f)), f
+    for i in range(w.size):  # contact slots beyond n_contacts are undefined
+        nc = int(rb.n_contacts[i])
+        assert np.array_equal(rb.contact_force[i, :nc], rs.contact_force[i, :nc])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    t = lambda a: torch.tensor(a, device=DEV)  # noqa: E731
+    wa, wb = scenarios.cfg4(20, start=0), scenarios.cfg4(20, start=20)
+    with torch.cuda.stream(s1):
+        ra = big.solve_static_batch(t(wa.x0), t(wa.tensions), t(wa.applied), tol=wa.tol, max_frames=wa.max_frames,
+                                    stream=s1)
+    with torch.cuda.stream(s2):
+        rb2 = big.solve_static_batch(t(wb.x0), t(wb.tensions), t(wb.applied), tol=wb.tol, max_frames=wb.max_frames,
+                                     stream=s2)
+    torch.cuda.synchronize()
+    ref = big.solve_static_batch(t(np.concatenate([wa.x0, wb.x0])), t(np.concatenate([wa.tensions, wb.tensions])),
+                                 t(np.concatenate([wa.applied, wb.applied])), tol=wa.tol, max_frames=wa.max_frames)
+    torch.cuda.synchronize()
+    assert np.array_equal(ra.coords.cpu().numpy(), ref.coords[:20].cpu().numpy())
+    assert np.array_equal(rb2.coords.cpu().numpy(), ref.coords[20:].cpu().numpy())
+
+
+def test_batch_inputs_are_validated():
+    """float32 / CPU-torch / wrong-shape inputs are converted or rejected, never passed as raw pointers."""
+    from paper_2503_06922_b200.engine import Engine
+    from paper_2503_06922_b200.errors import DomainError
+    w = scenarios.cfg3p(2)
+    eng = Engine(**w.engine_kwargs(), device=0)
+    ref = eng.solve_static_batch(torch.tensor(w.x0, device=DEV), None, torch.tensor(w.applied, device=DEV),
+                                 tol=w.tol, max_frames=w.max_frames).to_numpy()
+    r32 = eng.solve_static_batch(torch.tensor(w.x0, dtype=torch.float32, device=DEV).double(), None,
+                                 torch.tensor(w.applied), tol=w.tol, max_frames=w.max_frames).to_numpy()
+    assert np.array_equal(ref.coords, r32.coords)  # CPU-torch applied moved to the device
+    with pytest.raises(DomainError):
+        eng.solve_static_batch(torch.tensor(w.x0[:, :-6], device=DEV), None, None)
+    with pytest.raises(DomainError):
+        eng.solve_static_batch(torch.tensor(w.x0, device=DEV), None, torch.tensor(w.applied[:1], device=DEV))
