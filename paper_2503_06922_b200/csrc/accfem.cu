@@ -422,6 +422,8 @@ extern "C" int accfem_create(const accfem_model_desc* md, const accfem_mesh_desc
         }
       }
     }
+    // development knob: ACCFEM_SMEM_PAD=<doubles> pads the hot set (fewer teams per SM)
+    if (const char* pad = getenv("ACCFEM_SMEM_PAD")) hot = (hot + atol(pad) + 15) & ~15L;
     const bool in_smem = hot * 8 <= max_smem && !(force_global && force_global[0] == '1');
     if (!in_smem) h->hot_rows = 0;
     h->hot_stride = in_smem ? hot : 0;

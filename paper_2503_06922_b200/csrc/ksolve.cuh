@@ -48,33 +48,43 @@ __global__ void __launch_bounds__(32 * NW, 1)
   if (threadIdx.x < PF_COUNT) prof_acc[threadIdx.x] = 0;
   ws.prof = B.prof ? prof_acc : nullptr;
   __syncthreads();
-  const bool rec = B.team_stats && wid < B.team_stats_cap && threadIdx.x == 0;
-  unsigned long long t_start = 0, busy = 0;
-  long long solved = 0;
-  if (rec) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  // load-balance record (optional): kept in shared memory, not in registers
+  // that would stay live across the inlined solve
+  __shared__ unsigned long long lb[3];  // start ns, busy ns, scenarios
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    lb[0] = t;
+    lb[1] = 0;
+    lb[2] = 0;
+  }
   while (true) {
     if (threadIdx.x == 0) next = atomicAdd(B.work_counter, 1);
     __syncthreads();
     const int s = next;
     __syncthreads();
     if (s >= B.S) break;
-    unsigned long long t0 = 0, t1 = 0;
-    if (rec) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (threadIdx.x == 0 && B.team_stats) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      lb[1] -= t;
+    }
     run_scenario(team, P, B, s, ws);
-    if (rec) {
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      busy += t1 - t0;
-      ++solved;
+    if (threadIdx.x == 0 && B.team_stats) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      lb[1] += t;
+      lb[2] += 1;
     }
   }
   __syncthreads();
-  if (rec) {
+  if (threadIdx.x == 0 && B.team_stats && wid < B.team_stats_cap) {
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
     long long* o = B.team_stats + 4 * wid;
-    o[0] = solved;
-    o[1] = (long long)busy;
-    o[2] = (long long)t_start;
+    o[0] = (long long)lb[2];
+    o[1] = (long long)lb[1];
+    o[2] = (long long)lb[0];
     o[3] = (long long)t_end;
   }
   if (B.prof && threadIdx.x < PF_COUNT) B.prof[wid * PF_COUNT + threadIdx.x] = prof_acc[threadIdx.x];

@@ -608,11 +608,21 @@ DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
 template <class Team>
 DEV void dense_combine(const Team& team, int n, int na, const int* alist, const double* W, const double* y,
                        const double* base, double* out) {
-  parfor4(team, n, [&](int j) {
+  // W lives in the team's global slab: the loads of eight columns are issued
+  // together (memory-level parallelism), the sum keeps the sequential order
+  PARFOR(j, n) {
     double acc = base[j];
-    for (int q = 0; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
+    int q = 0;
+    for (; q + 8 <= na; q += 8) {
+      double w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = W[(long)alist[q + u] * n + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc -= y[q + u] * w[u];
+    }
+    for (; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
     out[j] = acc;
-  });
+  }
   team.sync();
 }
 
