@@ -95,3 +95,15 @@ def test_oracle_cfg4_samples_match_reference(golden):
     w = scenarios.cfg4(16)
     for i, got in enumerate(O.solve_workload(w, indices=range(0, 16, 3))):
         compare_solve(g, f"cfg4_{3 * i}", got)
+
+
+def test_reference_runner_matches_reference_status_and_frames(golden):
+    """oracle/reference_runner.py (the bench's CPU arm) drives the unmodified reference
+    from baseline/_ref: cfg3p solves (status 0) and the infeasible press reports status 5."""
+    import pytest
+    from oracle import reference_runner
+    from paper_2503_06922_b200 import scenarios
+    if not reference_runner.available():
+        pytest.skip("baseline/_ref not installed")
+    assert reference_runner.run_static(scenarios.cfg3p(1), 0) == 0
+    assert reference_runner.run_static(scenarios.infeasible_press(1), 0) == 5
