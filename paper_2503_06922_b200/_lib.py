@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaccfem.so")
+LIB_PATH = os.environ.get("ACCFEM_LIB") or os.path.join(HERE, "libaccfem.so")  # ACCFEM_LIB: development A/B builds
 
 c_int32, c_double, c_void_p = ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 

@@ -608,21 +608,11 @@ DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
 template <class Team>
 DEV void dense_combine(const Team& team, int n, int na, const int* alist, const double* W, const double* y,
                        const double* base, double* out) {
-  // W lives in the team's global slab: the loads of eight columns are issued
-  // together (memory-level parallelism), the sum keeps the sequential order
-  PARFOR(j, n) {
+  parfor4(team, n, [&](int j) {
     double acc = base[j];
-    int q = 0;
-    for (; q + 8 <= na; q += 8) {
-      double w[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) w[u] = W[(long)alist[q + u] * n + j];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc -= y[q + u] * w[u];
-    }
-    for (; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
+    for (int q = 0; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
     out[j] = acc;
-  }
+  });
   team.sync();
 }
 
@@ -876,7 +866,7 @@ DEV int pgs_sweeps(const Team& team, int nc, const double* W, const double* q0, 
 
 // not inlined: the comparison backend keeps its registers out of the hot kernel's allocation
 template <class Team>
-DEVNI int solve_pgs(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
+DEV int solve_pgs(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpResult& res, int cmax) {
   const int N = P.m.N, n = 6 * N, nf = F.nf, nc = F.nc;
   const int* frd = P.m.fixed_row_of_dof;
   if (nc > cmax) return ST_CAPACITY;
