@@ -1,13 +1,16 @@
 // B200 (sm_100a) device library behind include/accfem.h.
 //
-// Kernels (all FP64, one warp = one scenario, persistent over a dynamic
-// scenario queue):
+// Kernels (all FP64; the solve kernels are persistent over a dynamic scenario
+// queue, one CTA team = one scenario):
 //   k_model_setup     per-model constants (once per handle)
-//   k_solve           run_static / step for a batch: element pass, detection,
-//                     assembly, Ruiz, block Cholesky, ADMM, polish, update
+//   k_solve<NW, CR>   run_static / step for a batch: element pass, detection,
+//                     assembly, Ruiz, block-tridiagonal factorisation, ADMM or
+//                     PGS, polish, update -- 2-warp teams (throughput), 4-warp
+//                     teams, or 8-warp teams with cyclic reduction (latency)
 //   k_element_pass    unit entry point: F_int + block-tridiagonal K
 //   k_detect          unit entry point: per-node contact winner
-//   k_grid_*          broad-phase grid build over the lumen mesh (grid.cuh)
+//   k_grid_*          broad-phase grid build over the lumen mesh (grid.cuh; the
+//                     cell lists are sorted with cub's segmented sort)
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
