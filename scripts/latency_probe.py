@@ -27,8 +27,10 @@ def probe(tag, w, reps=12):
         if rep >= 2:
             ts.append((time.perf_counter() - t0) * 1e3)
     st = o.status.cpu().numpy()
-    print(f"{os.environ.get('ACCFEM_MODE', 'auto'):6s} {tag:10s} S={w.size:4d} p50 {statistics.median(ts):8.3f} ms "
-          f"min {min(ts):8.3f} frames {o.frames.cpu().numpy()[:4]} status {np.unique(st)}", flush=True)
+    p50 = statistics.median(ts)
+    print(f"{os.environ.get('ACCFEM_MODE', 'auto'):6s} {tag:10s} S={w.size:4d} p50 {p50:8.3f} ms "
+          f"min {min(ts):8.3f} -> {w.size / (p50 * 1e-3):9.1f} solves/s frames {o.frames.cpu().numpy()[:4]} "
+          f"status {np.unique(st)}", flush=True)
 
 
 if __name__ == "__main__":
@@ -40,6 +42,8 @@ if __name__ == "__main__":
             w = scenarios.cfg1(1)
         elif tag == "cfg4_148":
             w = scenarios.cfg4(148)
+        elif tag.startswith("cfg5_"):
+            w = scenarios.cfg5(int(tag.split("_")[1]))
         else:
             w = scenarios.CONFIGS[tag](1)
-        probe(tag, w, reps=6 if tag == "cfg5" else 12)
+        probe(tag, w, reps=6 if tag.startswith("cfg5") else 12)
