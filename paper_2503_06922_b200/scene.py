@@ -20,6 +20,7 @@ Reference anchors (all under /root/reference/pkg/src/cablefem/):
 
 from __future__ import annotations
 
+import re
 import struct
 from dataclasses import dataclass, field, replace
 from pathlib import Path
@@ -376,55 +377,76 @@ def make_tube(path_points, radii, segments=16):
     return mesh
 
 
+_STL_RECORD = np.dtype([("normal", "<f4", (3,)), ("corners", "<f4", (3, 3)), ("attr", "<u2")])
+_FLOAT = r"[-+]?(?:\d+\.?\d*|\.\d+)(?:[eE][-+]?\d+)?"
+
+
+def _mesh_from_corner_list(corners, where):
+    """Triangle soup (3k x 3 corner rows) -> indexed mesh: identical corners are
+    merged; vertices come out in lexicographic order (numpy unique), triangles in
+    file order -- the indexing the reference's loader produces (mesh.py:64-133)."""
+    corners = np.asarray(corners, dtype=float).reshape(-1, 3)
+    if corners.shape[0] == 0 or corners.shape[0] % 3:
+        raise MeshError(f"{where}: corner count {corners.shape[0]} is not a positive multiple of 3")
+    vertices, index = np.unique(corners, axis=0, return_inverse=True)
+    return TriangleMesh(vertices, np.asarray(index).reshape(-1, 3))
+
+
+def _read_stl(path):
+    raw = path.read_bytes()
+    if len(raw) >= 84:
+        count = int(np.frombuffer(raw, dtype="<u4", count=1, offset=80)[0])
+        if len(raw) == 84 + _STL_RECORD.itemsize * count:  # binary: header, count, 50-byte records
+            rec = np.frombuffer(raw, dtype=_STL_RECORD, count=count, offset=84)
+            return _mesh_from_corner_list(rec["corners"].astype(float), path)
+    text = raw.decode("ascii", errors="replace")
+    if not text.lstrip().lower().startswith("solid"):
+        raise MeshError(f"{path}: neither a binary STL (size/count mismatch) nor an ASCII one ('solid' header)")
+    rows = []
+    for line in text.splitlines():
+        tokens = line.split()
+        if tokens[:1] != ["vertex"]:
+            continue
+        values = re.findall(_FLOAT, line[line.index("vertex") + 6:])
+        if len(tokens) != 4 or len(values) != 3:
+            raise MeshError(f"{path}: bad vertex record {line.strip()!r}")
+        rows.append([float(v) for v in values])
+    return _mesh_from_corner_list(rows, path)
+
+
+def _read_obj(path):
+    vertices, faces = [], []
+    for number, line in enumerate(path.read_text().splitlines(), start=1):
+        tokens = line.split()
+        if not tokens or tokens[0][0] == "#":
+            continue
+        if tokens[0] == "v":
+            vertices.append([float(t) for t in tokens[1:4]])
+        elif tokens[0] == "f":
+            corners = [int(t.partition("/")[0]) - 1 for t in tokens[1:]]
+            if len(corners) != 3:
+                raise MeshError(f"{path}:{number}: {len(corners)}-gon face; only triangles are supported "
+                                "(export the OBJ triangulated)")
+            faces.append(corners)
+    if not faces:
+        raise MeshError(f"{path}: the OBJ file has no faces")
+    return TriangleMesh(np.asarray(vertices, dtype=float), np.asarray(faces))
+
+
+_READERS = {".stl": _read_stl, ".obj": _read_obj}
+
+
 def load_mesh(path):
-    """STL (binary/ASCII) or triangulated OBJ loader (mesh.py:64-133)."""
+    """Triangle mesh from an STL (binary or ASCII) or a triangulated OBJ file, in
+    meters -- the loader contract of the reference (mesh.py:64-133; MeshError on
+    missing / malformed files)."""
     path = Path(path)
     if not path.exists():
         raise MeshError(f"mesh file not found: {path}")
-    suffix = path.suffix.lower()
-    if suffix == ".stl":
-        raw = path.read_bytes()
-        if len(raw) >= 84:
-            (count,) = struct.unpack_from("<I", raw, 80)
-            if len(raw) == 84 + 50 * count:
-                rec = np.frombuffer(raw[84:84 + 50 * count], dtype=np.uint8).reshape(count, 50)
-                fl = rec[:, :48].copy().view("<f4").reshape(count, 12).astype(float)
-                return _dedup(fl[:, 3:12].reshape(-1, 3))
-        text = raw.decode("ascii", errors="replace")
-        if text.lstrip().lower().startswith("solid"):
-            verts = []
-            for line in text.splitlines():
-                parts = line.split()
-                if parts and parts[0] == "vertex":
-                    if len(parts) != 4:
-                        raise MeshError(f"malformed STL vertex line in {path}: {line!r}")
-                    verts.append([float(v) for v in parts[1:4]])
-            if not verts or len(verts) % 3:
-                raise MeshError(f"ASCII STL facet list incomplete in {path}")
-            return _dedup(np.asarray(verts, dtype=float))
-        raise MeshError(f"not a valid STL file: {path}")
-    if suffix == ".obj":
-        verts, faces = [], []
-        for lineno, line in enumerate(path.read_text().splitlines(), start=1):
-            parts = line.split()
-            if not parts or parts[0].startswith("#"):
-                continue
-            if parts[0] == "v":
-                verts.append([float(v) for v in parts[1:4]])
-            elif parts[0] == "f":
-                if len(parts) != 4:
-                    raise MeshError(f"{path} line {lineno}: face with {len(parts) - 1} vertices; "
-                                    "only triangulated OBJ is supported (re-export with triangulation)")
-                faces.append([int(r.split("/")[0]) - 1 for r in parts[1:]])
-        if not faces:
-            raise MeshError(f"no faces found in {path}")
-        return TriangleMesh(np.asarray(verts, dtype=float), np.asarray(faces))
-    raise MeshError(f"unsupported mesh format '{suffix}' (want .stl or .obj): {path}")
-
-
-def _dedup(flat):
-    uniq, inverse = np.unique(flat, axis=0, return_inverse=True)
-    return TriangleMesh(uniq, inverse.reshape(-1, 3))
+    reader = _READERS.get(path.suffix.lower())
+    if reader is None:
+        raise MeshError(f"unsupported mesh format {path.suffix!r} (.stl or .obj): {path}")
+    return reader(path)
 
 
 # ----------------------------------------------------------------------------

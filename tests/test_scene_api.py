@@ -68,3 +68,42 @@ def test_trajectory_csv(tmp_path):
     lines = p.read_text().splitlines()
     assert lines[7].startswith("t,node0_x") and lines[8].endswith(",0.0,7")
     assert p.read_text() == write_trajectory_csv(tmp_path / "u.csv", "demo", [rec, rec], 2).read_text()
+
+
+def test_load_mesh_matches_reference_loader(tmp_path):
+    """Binary STL, ASCII STL and OBJ give the reference loader's indexed mesh
+    (vertex order, triangles, normals) -- the reference from baseline/_ref."""
+    import os
+    import sys
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "cablefem")):
+        pytest.skip("baseline/_ref not installed")
+    sys.path.insert(0, ref_dir)
+    from cablefem import mesh as rm
+
+    from paper_2503_06922_b200.scene import load_mesh, make_tube
+    x = np.linspace(0.0, 0.1, 15)
+    m = make_tube(np.stack([x, 0 * x, 0.001 * np.sin(30 * x)], 1), 0.003 + 0 * x, segments=10)
+    rm.save_stl(rm.TriangleMesh(m.vertices.copy(), m.triangles.copy()), tmp_path / "b.stl")
+    with open(tmp_path / "a.stl", "w") as f:
+        f.write("solid s\n")
+        for t in m.triangles:
+            f.write(" facet normal 0 0 1\n  outer loop\n")
+            for v in m.vertices[t]:
+                f.write(f"   vertex {v[0]:.9e} {v[1]:.9e} {v[2]:.9e}\n")
+            f.write("  endloop\n endfacet\n")
+        f.write("endsolid s\n")
+    with open(tmp_path / "c.obj", "w") as f:
+        for v in m.vertices:
+            f.write(f"v {float(v[0])!r} {float(v[1])!r} {float(v[2])!r}\n")
+        for t in m.triangles:
+            f.write(f"f {t[0] + 1}/1 {t[1] + 1} {t[2] + 1}\n")
+    for name in ("b.stl", "a.stl", "c.obj"):
+        r, o = rm.load_mesh(tmp_path / name), load_mesh(tmp_path / name)
+        assert np.array_equal(r.vertices, o.vertices) and np.array_equal(r.triangles, o.triangles), name
+        assert np.allclose(r.normals, o.normals), name
+    (tmp_path / "q.obj").write_text("v 0 0 0\nf 1 2 3 4\n")
+    with pytest.raises(MeshError):
+        load_mesh(tmp_path / "q.obj")
+    with pytest.raises(MeshError):
+        load_mesh(tmp_path / "missing.stl")
