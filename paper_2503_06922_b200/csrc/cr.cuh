@@ -189,7 +189,8 @@ DEV double cr_root_row(const CrF& F, const double* vg, int r, const int* so) {
 // (rhs, block) items are spread over the groups; the top levels, whose items
 // fit in the five groups of warp 0, run on warp 0 alone with warp barriers.
 // In the backward sweep a group reads all of v_i before any lane writes x_i.
-static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, CrF F, double* v, int nrhs, long stride) {
+static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, CrF F, double* v, int nrhs, long stride,
+                                                     const int* rhs_block = nullptr) {
   const int Lv = cr_levels(N);
   const int lane = team.w.lane, grp = lane / 6, r = lane - 6 * grp;
   const bool glane = lane < 30;
@@ -206,12 +207,44 @@ static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, 
   CR_T(0);
   for (int l = 0; l < ltop; ++l) {
     const int s = 1 << l, ns = cr_surv_count(N, l);
+    // two items per group per pass: both rows' loads are in flight before
+    // either store (items of one level never touch each other's rows)
+    // rhs_block: right-hand side g is zero outside block rhs_block[g], so after
+    // this level it is zero outside the (at most two) survivors j with
+    // |j - rhs_block[g]| < 2s; the other survivors' rows are exact zeros and
+    // are skipped (identical results, O(log N) forward items per right-hand side)
+    const int items = rhs_block ? 2 * nrhs : nrhs * ns;
     if (glane)
-      for (int u = gid; u < nrhs * ns; u += ngr) {
-        const int g = nrhs == 1 ? 0 : u / ns, q = u - g * ns;
-        double* vg = v + g * stride;
-        const int j = 2 * s * q;
-        vg[6 * j + r] = cr_fwd_row(N, F, vg, j, s, r);
+      for (int u0 = gid; u0 < items; u0 += 2 * ngr) {
+        double a[2];
+        double* dst[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int u = u0 + k * ngr;
+          dst[k] = nullptr;
+          if (u < items) {
+            int g, j;
+            bool live = true;
+            if (rhs_block) {
+              g = u >> 1;
+              const int kb = rhs_block[g], j0 = kb / (2 * s) * (2 * s);
+              j = j0 + (u & 1) * 2 * s;
+              live = (u & 1) == 0 || (kb > j0 && j / (2 * s) < ns);
+            } else {
+              const int q = nrhs == 1 ? u : u / nrhs;  // block-major: neighbouring groups share the factor rows
+              g = u - q * nrhs;
+              j = 2 * s * q;
+            }
+            if (live) {
+              double* vg = v + g * stride;
+              a[k] = cr_fwd_row(N, F, vg, j, s, r);
+              dst[k] = vg + 6 * j + r;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (dst[k]) *dst[k] = a[k];
       }
     team.sync();
     CR_T(1 + l);
@@ -287,15 +320,24 @@ static __device__ __noinline__ void cr_solve_inplace(const TeamCR& team, int N, 
   for (int l = ltop - 1; l >= 0; --l) {
     const int s = 1 << l, ne = cr_elim_count(N, l);
     const int items = nrhs * ne;
-    for (int b = 5 * team.warp; b < items; b += ngr) {
-      const int u = b + grp;
-      const bool act = glane && u < items;
-      const int g = nrhs == 1 ? 0 : u / ne, q = u - g * ne;
-      const int i = s + 2 * s * q;
-      double a = 0.0;
-      if (act) a = cr_bwd_row(N, F, v + g * stride, i, s, r, so);
+    for (int b = 5 * team.warp; b < items; b += 2 * ngr) {
+      double a[2];
+      double* dst[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int u = b + k * ngr + grp;
+        dst[k] = nullptr;
+        if (glane && u < items) {
+          const int q = nrhs == 1 ? u : u / nrhs, g = u - q * nrhs;  // block-major
+          const int i = s + 2 * s * q;
+          a[k] = cr_bwd_row(N, F, v + g * stride, i, s, r, so);
+          dst[k] = v + g * stride + 6 * i + r;
+        }
+      }
       __syncwarp();
-      if (act) v[g * stride + 6 * i + r] = a;
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (dst[k]) *dst[k] = a[k];
     }
     team.sync();
     CR_T(22 + l);
@@ -322,8 +364,8 @@ DEV void twisted_solve(const TeamCR& t, int N, const double* D, const double* U,
   cr_solve_inplace(t, N, cr_of(N, const_cast<double*>(D), U), out, nrhs, stride);
 }
 DEV void twisted_solve_chunks(const TeamCR& t, int N, const double* D, const double* U, double* rhs, int nrhs,
-                              long stride) {
-  cr_solve_inplace(t, N, cr_of(N, const_cast<double*>(D), U), rhs, nrhs, stride);
+                              long stride, const int* rhs_block = nullptr) {
+  cr_solve_inplace(t, N, cr_of(N, const_cast<double*>(D), U), rhs, nrhs, stride, rhs_block);
 }
 DEV bool dense_chol(const TeamCR& team, int na, double* S, double* col);
 #endif

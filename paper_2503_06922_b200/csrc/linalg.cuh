@@ -298,7 +298,8 @@ DEV void twisted_solve_multi(const TeamSerial& t, int N, const double* D, const 
 // block's right-hand side with its v (read first), the middle block's is
 // read before anything is written to it, z and x replace v in place.
 DEV void twisted_solve_chunks(const TeamSerial& t, int N, const double* D, const double* U, double* rhs, int nrhs,
-                              long stride) {
+                              long stride, const int* rhs_block = nullptr) {
+  (void)rhs_block;  // support hint used by the cyclic-reduction team only
   for (int c0 = 0; c0 < nrhs; c0 += kMultiRhs) {
     const int nb = nrhs - c0 < kMultiRhs ? nrhs - c0 : kMultiRhs;
     double* b = rhs + (long)c0 * stride;
@@ -889,7 +890,7 @@ DEV void twisted_solve_la(const TeamWarp& team, int N, const double* D, const do
 // products run across all lanes between the sweeps.  out may alias rhs.
 DEV void twisted_solve_multi(const TeamWarp& team, int N, const double* __restrict__ D,
                              const double* __restrict__ U, const double* rhs, double* tmp, double* out, int nrhs,
-                             long stride) {
+                             long stride, const int* rhs_block = nullptr) {
   const int lane = team.lane;
   const int g = lane >> 1;
   const bool top = (lane & 1) == 0;
@@ -900,12 +901,21 @@ DEV void twisted_solve_multi(const TeamWarp& team, int N, const double* __restri
   double* v = tmp + (act ? g : 0) * stride;
   double* x = out + (act ? g : 0) * stride;
   double p[6] = {0, 0, 0, 0, 0, 0};
+  // rhs_block (in-place solves only): right-hand side g is zero outside block
+  // rhs_block[g], so each half's elimination is exactly zero (and v = b there)
+  // until it reaches that block; the sweep starts there
+  int t0 = 0;
+  if (rhs_block && act) {
+    const int kb = rhs_block[g];
+    t0 = top ? kb : N - 1 - kb;
+    t0 = t0 < 0 ? 0 : (t0 > cnt ? cnt : t0);
+  }
   if (act) {
-    for (int t = 0; t < cnt; ++t) {
+    for (int t = t0; t < cnt; ++t) {
       const int i = top ? t : N - 1 - t;
       double a[6];
       ld6(b + 6 * i, a);
-      if (t > 0) {
+      if (t > t0) {
         double M[36];
         ld36(top ? U + 36 * (i - 1) : U + 36 * i, M);
 #pragma unroll
@@ -1004,11 +1014,11 @@ DEV void twisted_solve_multi(const TeamCta& t, int N, const double* D, const dou
 }
 // every warp of the team solves its own chunks of kMultiRhs right-hand sides, in place
 DEV void twisted_solve_chunks(const TeamCta& t, int N, const double* D, const double* U, double* rhs, int nrhs,
-                              long stride) {
+                              long stride, const int* rhs_block = nullptr) {
   for (int c0 = t.warp * kMultiRhs; c0 < nrhs; c0 += t.nw * kMultiRhs) {
     const int nb = nrhs - c0 < kMultiRhs ? nrhs - c0 : kMultiRhs;
     double* b = rhs + (long)c0 * stride;
-    twisted_solve_multi(t.w, N, D, U, b, b, b, nb, stride);
+    twisted_solve_multi(t.w, N, D, U, b, b, b, nb, stride, rhs_block ? rhs_block + c0 : nullptr);
   }
   t.sync();
 }

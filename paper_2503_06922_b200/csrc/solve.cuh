@@ -524,10 +524,35 @@ DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
       col[r] = v;
     }
     team.sync();
-    for (int r = k + 1 + team.warp; r < na; r += team.nw) {
-      const double cr = col[r];
-      double* Sr = S + (long)r * na;
-      for (int cc = k + 1 + team.w.lane; cc <= r; cc += 32) Sr[cc] -= cr * col[cc];
+    // four rows per warp and two column chunks per lane per pass: up to eight
+    // independent S loads in flight (S is L2-resident at these sizes; one row
+    // at a time left every warp waiting on one L2 round trip per row)
+    for (int r0 = k + 1 + team.warp; r0 < na; r0 += 4 * team.nw) {
+      int rr[4];
+      double crr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        rr[i] = r0 + i * team.nw;
+        crr[i] = rr[i] < na ? col[rr[i]] : 0.0;
+      }
+      const int rmax = rr[3] < na ? rr[3] : na - 1;
+      for (int cc = k + 1 + team.w.lane; cc <= rmax; cc += 64) {
+        const int c2 = cc + 32;
+        const double x0 = col[cc], x1 = c2 <= rmax ? col[c2] : 0.0;
+        double a0[4], a1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool in = rr[i] < na;
+          a0[i] = in && cc <= rr[i] ? S[(long)rr[i] * na + cc] : 0.0;
+          a1[i] = in && c2 <= rr[i] ? S[(long)rr[i] * na + c2] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool in = rr[i] < na;
+          if (in && cc <= rr[i]) S[(long)rr[i] * na + cc] = a0[i] - crr[i] * x0;
+          if (in && c2 <= rr[i]) S[(long)rr[i] * na + c2] = a1[i] - crr[i] * x1;
+        }
+      }
     }
     team.sync();
   }
@@ -608,11 +633,51 @@ DEV void dense_solve(const Team& team, int na, const double* S, double* b) {
 template <class Team>
 DEV void dense_combine(const Team& team, int n, int na, const int* alist, const double* W, const double* y,
                        const double* base, double* out) {
-  parfor4(team, n, [&](int j) {
-    double acc = base[j];
-    for (int q = 0; q < na; ++q) acc -= y[q] * W[(long)alist[q] * n + j];
-    out[j] = acc;
-  });
+  // four columns per thread, four contacts per pass: 16 independent W loads in
+  // flight (the W panel is L2/HBM-resident for large N); each column still
+  // accumulates in contact order
+  const int s = team.size();
+  for (int j0 = team.rank(); j0 < n; j0 += 4 * s) {
+    int jj[4];
+    double acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      jj[u] = j0 + u * s < n ? j0 + u * s : n - 1;
+      acc[u] = base[jj[u]];
+    }
+    int q = 0;
+    for (; q + 4 <= na; q += 4) {
+      const double* w0 = W + (long)alist[q] * n;
+      const double* w1 = W + (long)alist[q + 1] * n;
+      const double* w2 = W + (long)alist[q + 2] * n;
+      const double* w3 = W + (long)alist[q + 3] * n;
+      const double y0 = y[q], y1 = y[q + 1], y2 = y[q + 2], y3 = y[q + 3];
+      double e0[4], e1[4], e2[4], e3[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        e0[u] = w0[jj[u]];
+        e1[u] = w1[jj[u]];
+        e2[u] = w2[jj[u]];
+        e3[u] = w3[jj[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u] -= y0 * e0[u];
+        acc[u] -= y1 * e1[u];
+        acc[u] -= y2 * e2[u];
+        acc[u] -= y3 * e3[u];
+      }
+    }
+    for (; q < na; ++q) {
+      const double* wq = W + (long)alist[q] * n;
+      const double yq = y[q];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] -= yq * wq[jj[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u * s < n) out[j0 + u * s] = acc[u];
+  }
   team.sync();
 }
 
@@ -645,7 +710,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     }
   }
   team.sync();
-  twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, nc, n);
+  twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, nc, n, ws.cnode);
   PARFOR(t, nc * nc) {
     const int p = t / nc, q = t - p * nc;
     const double* nr = ws.cnrm + 3 * p;
@@ -667,6 +732,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
   PROF_T0(t_pr);
   for (int round = 0; round < 6; ++round) {
     res.polish_rounds = round + 1;
+    PROF_T0(t_r0);
     // active contact list in row order
     int na = 0;
     for (int base = 0; base < nc; base += team.size()) {
@@ -681,6 +747,8 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     PARFOR(q, na) ws.alist[N + ws.alist[q]] = q;
     team.sync();
     if (nf + na == 0) break;
+    PROF_ADD(ws, PF_PR_LIST, t_r0);
+    PROF_T0(t_r1);
     // S_a = S[act, act] + delta I, factored
     PARFOR(t, na * na) {
       const int p = t / na, q = t - p * na;
@@ -695,7 +763,11 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     PARFOR(q, na) yact[q] = ws.Cv[ws.alist[q]] - ws.up[nf + ws.alist[q]];
     team.sync();
     if (na > 0) dense_solve(team, na, ws.S, yact);
+    PROF_ADD(ws, PF_PR_CHOL, t_r1);
+    PROF_T0(t_r2);
     dense_combine(team, n, na, ws.alist, ws.W, yact, ws.v, dxp);
+    PROF_ADD(ws, PF_PR_COMB, t_r2);
+    PROF_T0(t_r3);
     // one refinement round against the exact KKT (solver.py:514-522)
     block_matvec(team, N, ws.KD, ws.KU, dxp, ws.xt);
     PARFOR(j, n) {
@@ -711,6 +783,8 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     team.sync();
     twisted_solve(team, N, ws.HD, ws.HU, ws.xt, ws.tmp, ws.w, 1, 0, ws.sh);
     team.sync();
+    PROF_ADD(ws, PF_PR_REFINE, t_r3);
+    PROF_T0(t_r4);
     PARFOR(q, na) {
       const int c = ws.alist[q];
       const double r2 = ws.up[nf + c] - row_dot(P, F, ws, nf + c, dxp);
@@ -722,6 +796,8 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     PARFOR(j, n) dxp[j] += ws.colh[j];
     PARFOR(q, na) yact[q] += dyq[q];
     team.sync();
+    PROF_ADD(ws, PF_PR_CORR, t_r4);
+    PROF_T0(t_r5);
     // multipliers by row: selectors from the exact KKT, active contacts, 0 otherwise
     PARFOR(c, nc) yp[nf + c] = 0.0;
     team.sync();
@@ -737,6 +813,7 @@ DEV int polish(const Team& team, const Problem& P, const Frame& F, Ws& ws, QpRes
     neg = team.any(neg);
     viol = team.any(viol);
     team.sync();
+    PROF_ADD(ws, PF_PR_MULT, t_r5);
     if (!neg && !viol) {
       found = true;
       break;
@@ -892,7 +969,7 @@ DEV int solve_pgs(const Team& team, const Problem& P, const Frame& F, Ws& ws, Qp
       }
     }
     team.sync();
-    twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, nc, n);
+    twisted_solve_chunks(team, N, ws.HD, ws.HU, ws.W, nc, n, ws.cnode);
     // Delassus W_pq = C~_p W_q, q0 = C~ v - b_adj (b_adj removes the selector DOFs' prescribed part)
     PARFOR(t, nc * nc) {
       const int p = t / nc, q = t - p * nc;

@@ -49,7 +49,8 @@ DEV void parfor4(const Team& team, int n, F&& f) {
 #define PROF_ADD(ws, k, v)
 #endif
 enum ProfPhase { PF_ELEMENT = 0, PF_DETECT, PF_RUIZ, PF_FACTOR, PF_ITER, PF_CHAIN, PF_CHECK, PF_POLISH, PF_DIRECT,
-                 PF_POST, PF_TOTAL, PF_ITERS, PF_FRAMES, PF_POL_FACTOR, PF_POL_W, PF_POL_ROUNDS, PF_COUNT = 16 };
+                 PF_POST, PF_TOTAL, PF_ITERS, PF_FRAMES, PF_POL_FACTOR, PF_POL_W, PF_POL_ROUNDS,
+                 PF_PR_LIST, PF_PR_CHOL, PF_PR_COMB, PF_PR_REFINE, PF_PR_CORR, PF_PR_MULT, PF_COUNT = 24 };
 
 namespace accfem {
 

@@ -14,7 +14,7 @@ S = int(sys.argv[2]) if len(sys.argv) > 2 else 1776
 w = scenarios.cfg4(S) if name == "cfg4" else scenarios.CONFIGS[name](S)
 eng = Engine(**w.engine_kwargs(), device=0)
 teams = eng._lib.accfem_teams_resident(eng._h)
-prof = torch.zeros((teams, 16), dtype=torch.int64, device="cuda:0")
+prof = torch.zeros((teams, 24), dtype=torch.int64, device="cuda:0")
 assert eng._lib.accfem_dev_set_profile(eng._h, prof.data_ptr()) == 0
 t = lambda a: None if a is None else torch.tensor(a, device="cuda:0")
 torch.cuda.synchronize(); t0 = time.perf_counter()
@@ -29,3 +29,5 @@ for i, nm in enumerate(names[:11]):
 print(f"  per ADMM iteration: {p[4]/max(p[11],1):.0f} cycles (chain {p[5]/max(p[11],1):.0f})")
 print(f"  polish: factor {p[13]/S/1e6:.3f} W+S+v {p[14]/S/1e6:.3f} rounds {p[15]/S/1e6:.3f} Mcycles/solve")
 print(f"  per frame: element {p[0]/max(p[12],1):.0f} detect {p[1]/max(p[12],1):.0f} ruiz {p[2]/max(p[12],1):.0f} factor {p[3]/max(p[12],1):.0f} polish {p[7]/max(p[12],1):.0f}")
+print(f"  polish round parts (Mcycles/solve): list {p[16]/S/1e6:.3f} chol+solve {p[17]/S/1e6:.3f} combine {p[18]/S/1e6:.3f} "
+      f"refine {p[19]/S/1e6:.3f} correction {p[20]/S/1e6:.3f} multipliers {p[21]/S/1e6:.3f}")
