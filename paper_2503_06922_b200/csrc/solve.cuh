@@ -505,53 +505,82 @@ DEV void dense_solve_warp(const TeamWarp& w, int na, const double* S, double* b)
 }
 // up to this many active contacts the Schur factor/solves run on one warp;
 // larger systems (the 1000-node configs: 200-250 contacts) use the whole team,
-// the scaled column copied to the contiguous `col` and the trailing lower
-// triangle updated one row per warp with the lanes along the row (coalesced)
+// the scaled column copied to the contiguous `col`, the trailing lower triangle
+// updated in panels with the lanes along a row (coalesced)
 constexpr int kDenseWarpMax = 64;
 DEV bool dense_chol(const TeamCta& team, int na, double* S, double* col) {
   team.sync();  // S assembled by the whole team
   if (na <= kDenseWarpMax)
     return team.on_warp0([&](const TeamWarp& w) { return dense_chol_warp(w, na, S) ? 1 : 0; }) != 0;
-  for (int k = 0; k < na; ++k) {
-    double piv = S[k * na + k];
-    if (!(piv > 0.0)) return false;
-    double l = sqrt(piv);
-    team.sync();
-    PARFOR(i, na - k) {
-      const int r = k + i;
-      const double v = (r == k) ? l : S[r * na + k] / l;
-      S[r * na + k] = v;
-      col[r] = v;
+  // Right-looking, in panels of kPanel columns: inside a panel the columns are
+  // factored one by one (a thread per row updates its panel entries); the
+  // trailing matrix then takes the panel's kPanel updates in one pass per entry,
+  // in column order -- every entry sees the same fused multiply-adds in the same
+  // order as the column-by-column algorithm, with one L2 round trip per panel
+  // instead of per column.
+  constexpr int kPanel = 8;
+  for (int k0 = 0; k0 < na; k0 += kPanel) {
+    const int k1 = k0 + kPanel < na ? k0 + kPanel : na;
+    for (int k = k0; k < k1; ++k) {
+      const double piv = S[k * na + k];
+      if (!(piv > 0.0)) return false;
+      const double l = sqrt(piv);
+      team.sync();
+      PARFOR(i, na - k) {
+        const int r = k + i;
+        const double v = (r == k) ? l : S[r * na + k] / l;
+        S[r * na + k] = v;
+        col[r] = v;
+      }
+      team.sync();
+      // panel columns c in (k, k1), rows r >= c
+      PARFOR(i, na - k - 1) {
+        const int r = k + 1 + i;
+        const double cr = col[r];
+        double* Sr = S + (long)r * na;
+        double a[kPanel - 1], x[kPanel - 1];
+#pragma unroll
+        for (int j = 0; j < kPanel - 1; ++j) {
+          const int c = k + 1 + j;
+          const bool in = c < k1 && c <= r;
+          a[j] = in ? Sr[c] : 0.0;
+          x[j] = in ? col[c] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kPanel - 1; ++j) {
+          const int c = k + 1 + j;
+          if (c < k1 && c <= r) Sr[c] = a[j] - cr * x[j];
+        }
+      }
+      team.sync();
     }
-    team.sync();
-    // four rows per warp and two column chunks per lane per pass: up to eight
-    // independent S loads in flight (S is L2-resident at these sizes; one row
-    // at a time left every warp waiting on one L2 round trip per row)
-    for (int r0 = k + 1 + team.warp; r0 < na; r0 += 4 * team.nw) {
+    // trailing entries (r, c), k1 <= c <= r: four rows per warp, lanes along c
+    for (int r0 = k1 + team.warp; r0 < na; r0 += 4 * team.nw) {
       int rr[4];
-      double crr[4];
+      double lr[4][kPanel];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         rr[i] = r0 + i * team.nw;
-        crr[i] = rr[i] < na ? col[rr[i]] : 0.0;
+#pragma unroll
+        for (int t = 0; t < kPanel; ++t)
+          lr[i][t] = rr[i] < na && k0 + t < k1 ? S[(long)rr[i] * na + k0 + t] : 0.0;
       }
       const int rmax = rr[3] < na ? rr[3] : na - 1;
-      for (int cc = k + 1 + team.w.lane; cc <= rmax; cc += 64) {
-        const int c2 = cc + 32;
-        const double x0 = col[cc], x1 = c2 <= rmax ? col[c2] : 0.0;
-        double a0[4], a1[4];
+      for (int cc = k1 + team.w.lane; cc <= rmax; cc += 32) {
+        double lc[kPanel], a[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const bool in = rr[i] < na;
-          a0[i] = in && cc <= rr[i] ? S[(long)rr[i] * na + cc] : 0.0;
-          a1[i] = in && c2 <= rr[i] ? S[(long)rr[i] * na + c2] : 0.0;
-        }
+        for (int t = 0; t < kPanel; ++t) lc[t] = k0 + t < k1 ? S[(long)cc * na + k0 + t] : 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const bool in = rr[i] < na;
-          if (in && cc <= rr[i]) S[(long)rr[i] * na + cc] = a0[i] - crr[i] * x0;
-          if (in && c2 <= rr[i]) S[(long)rr[i] * na + c2] = a1[i] - crr[i] * x1;
-        }
+        for (int i = 0; i < 4; ++i) a[i] = rr[i] < na && cc <= rr[i] ? S[(long)rr[i] * na + cc] : 0.0;
+#pragma unroll
+        for (int t = 0; t < kPanel; ++t)
+          if (k0 + t < k1) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = a[i] - lr[i][t] * lc[t];
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (rr[i] < na && cc <= rr[i]) S[(long)rr[i] * na + cc] = a[i];
       }
     }
     team.sync();

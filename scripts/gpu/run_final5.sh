@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python scripts/ab_bitexact.py oldsrc/paper_2503_06922_b200/libaccfem.so paper_2503_06922_b200/libaccfem.so > gpurun_out/f5_ab.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/f5_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/f5_pytest.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f5_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/f5_smoke.log
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/f5_bench.log 2>&1; echo "rc=$?" >> gpurun_out/f5_bench.log
