@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/f6_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/f6_pytest.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f6_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/f6_smoke.log

@@ -175,12 +175,13 @@ def test_single_scenario_api_raises_reference_exception_classes():
 
 
 @pytest.mark.parametrize("mode", ["cr", "team4", "team2"])
-@pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg2", "cfg4"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg3p", "cfg3", "cfg2", "cfg4", "cfg5"])
 def test_every_kernel_mode_matches_reference_goldens(golden, name, mode, monkeypatch):
-    """The three k_solve variants -- latency mode (one 16-warp CTA per scenario,
+    """The three k_solve variants -- latency mode (one 8-warp CTA per scenario,
     cyclic reduction), 4-warp teams and 2-warp throughput teams (twisted LDL^T)
     -- forced for any batch size, each against the reference goldens with
-    per-frame ADMM iteration counts."""
+    per-frame ADMM iteration counts.  cfg5 (N = 1001, ~200 active contacts) runs
+    the global-workspace layout and the team-wide panel Schur Cholesky."""
     monkeypatch.setenv("ACCFEM_MODE", mode)
     g = golden("solves.npz")
     if name == "cfg1":
