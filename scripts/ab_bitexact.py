@@ -42,7 +42,7 @@ def main():
         run(sys.argv[2])
         return
     outs = []
-    for i, so in enumerate(sys.argv[1:3]):
+    for i, so in enumerate(os.path.abspath(p) for p in sys.argv[1:3]):  # dlopen needs a path, not a bare name
         out = f"/tmp/ab_{i}.npz"
         subprocess.run([sys.executable, __file__, "--run", out], check=True, env={**os.environ, "ACCFEM_LIB": so})
         outs.append(np.load(out))
