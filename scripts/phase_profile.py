@@ -11,7 +11,10 @@ _lib._LIB.accfem_dev_set_profile.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 from paper_2503_06922_b200.engine import Engine
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 1776
-w = scenarios.cfg4(S) if name == "cfg4" else scenarios.CONFIGS[name](S)
+if name.startswith("c400_"):  # criterion-6 constriction scenes (400 nodes, 5 or 50 contacts)
+    w = scenarios.constriction(400, int(name[5:]), name, n_scenarios=S)
+else:
+    w = scenarios.cfg4(S) if name == "cfg4" else scenarios.CONFIGS[name](S)
 eng = Engine(**w.engine_kwargs(), device=0)
 teams = eng._lib.accfem_teams_resident(eng._h)
 prof = torch.zeros((teams, 24), dtype=torch.int64, device="cuda:0")
